@@ -1,0 +1,304 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, obviously-correct fp64 CPU reference for the AsyFLEXA hot path
+of Cannelli, Facchinei, Kungurtsev, Scutari, "Asynchronous Parallel Algorithms
+for Nonconvex Big-Data Optimization, Part II" (arXiv:1701.04900), PAPER.md.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this module.  It
+shares no code with the CUDA path (``paper_1701_04900_b200/csrc``); the only
+common dependency is the seeded input recipe ``paper_1701_04900_b200.inputs``,
+which holds none of the method's arithmetic.
+
+Every function cites the PAPER.md passage it writes out.  Conventions
+(readings R1..R12 in DESIGN.md):
+  * problem (1) [PAPER.md:58-68]: F = f + G, G = lam*||x||_1 (or the DC
+    regularizers of Eq. 12), X_i = [lo, hi]^{n_i}, no nonconvex c_{j_i}.
+  * f = s*||Ax-b||^2 - c*||x||^2 (LASSO: s = 1/2 [PAPER.md:433]; Eq. 11: s = 1
+    [PAPER.md:523]) or the l1-logistic loss (1/m) sum log(1+exp(-y_j a_j^T x)).
+  * surrogate: proximal-linear, tilde f_i(x_i; y) = grad_i f(y)^T (x_i - y_i)
+    + 1/2 sum_{j in block i} tau_j (x_j - y_j)^2 -- satisfies Assumption B
+    [PAPER.md:166-179]; for scalar blocks of a quadratic with tau_j = q_j it is
+    the paper's Sec. 4.1 surrogate f(x_i; x_{-i}) (+ tau^k/2 (.)^2, tau^k = 0)
+    [PAPER.md:437].
+
+Parity status: every function here is pinned by ``tests/test_oracle_pins.py``
+(closed forms, brute force, finite differences, sklearn, KKT invariants);
+none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import math
+from typing import Iterable, Optional
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.special import expit
+
+# ----------------------------------------------------------------------------
+# data access (A as a linear operator; dense ndarray or scipy CSC)
+# ----------------------------------------------------------------------------
+
+
+def design(P):
+    """A as a dense ndarray or a scipy CSC matrix (library primitive)."""
+    if P.kind == "dense":
+        return P.A
+    return sp.csc_matrix((P.vals, P.rowidx, P.colptr), shape=(P.m, P.n))
+
+
+def columns(P, j0: int, j1: int):
+    """A_i = columns j0..j1-1 of A (dense ndarray)."""
+    if P.kind == "dense":
+        return P.A[:, j0:j1]
+    return design(P)[:, j0:j1].toarray()
+
+
+def lo_hi(P):
+    lo = np.broadcast_to(np.asarray(P.lo, float), (P.n,))
+    hi = np.broadcast_to(np.asarray(P.hi, float), (P.n,))
+    return lo, hi
+
+
+# ----------------------------------------------------------------------------
+# f, G, F  -- problem (1) [PAPER.md:58-68], LASSO [PAPER.md:433], Eq. (11) [PAPER.md:521-525]
+# ----------------------------------------------------------------------------
+
+
+def smooth_value(P, x: np.ndarray) -> float:
+    """f(x).  LS: s*||Ax-b||^2 - c||x||^2.  Logistic: mean log(1+exp(-y Ax)) - c||x||^2."""
+    z = design(P) @ x
+    if P.loss == "ls":
+        r = z - P.b
+        val = P.scale * float(r @ r)
+    else:
+        val = float(np.mean(np.logaddexp(0.0, -P.b * z)))
+    return val - P.c * float(x @ x)
+
+
+def smooth_grad(P, x: np.ndarray) -> np.ndarray:
+    """grad f(x) by definition.  LS: 2s A^T(Ax-b) - 2c x.
+    Logistic: A^T w - 2c x, w_j = -(y_j/m) sigmoid(-y_j (Ax)_j)."""
+    A = design(P)
+    z = A @ x
+    if P.loss == "ls":
+        w = 2.0 * P.scale * (z - P.b)
+    else:
+        w = -(P.b / P.m) * expit(-P.b * z)
+    return A.T @ w - 2.0 * P.c * x
+
+
+# --- DC regularizers of Sec. 4.3, Eq. (12) [PAPER.md:526-533] -------------------
+
+
+def h(P, t):
+    """scalar penalty h: |t| (l1), 1-exp(-theta|t|) (exp), log(1+theta|t|)/log(1+theta) (log)."""
+    t = np.abs(t)
+    if P.reg == "l1":
+        return t
+    if P.reg == "exp":
+        return 1.0 - np.exp(-P.theta * t)
+    return np.log1p(P.theta * t) / math.log1p(P.theta)
+
+
+def eta(P) -> float:
+    """eta(theta): exp -> theta, log -> theta/log(1+theta) [PAPER.md:532]; l1 -> 1."""
+    if P.reg == "l1":
+        return 1.0
+    if P.reg == "exp":
+        return P.theta
+    return P.theta / math.log1p(P.theta)
+
+
+def h_plus(P, t):
+    return eta(P) * np.abs(t)
+
+
+def h_minus(P, t):
+    """h^-(t) = eta|t| - h(t) (Eq. 12)."""
+    return eta(P) * np.abs(t) - h(P, t)
+
+
+def grad_h_minus(P, t):
+    """d/dt h^-(t): exp: eta*sign(t)*(1-exp(-theta|t|)); log: sign(t)*(eta - theta/((1+theta|t|)log(1+theta)))."""
+    t = np.asarray(t, float)
+    if P.reg == "l1":
+        return np.zeros_like(t)
+    if P.reg == "exp":
+        return eta(P) * np.sign(t) * (1.0 - np.exp(-P.theta * np.abs(t)))
+    return np.sign(t) * (eta(P) - P.theta / ((1.0 + P.theta * np.abs(t)) * math.log1p(P.theta)))
+
+
+def G(P, x: np.ndarray) -> float:
+    """G(x) = lam*sum_i h(x_i) on the box, +inf outside X."""
+    lo, hi = lo_hi(P)
+    if np.any(x < lo) or np.any(x > hi):
+        return math.inf
+    return P.lam * float(np.sum(h(P, x)))
+
+
+def objective(P, x: np.ndarray) -> float:
+    """F(x) = f(x) + G(x), Eq. (1) [PAPER.md:60]."""
+    return smooth_value(P, x) + G(P, x)
+
+
+# ----------------------------------------------------------------------------
+# best response, Eq. (2) [PAPER.md:148-152]
+# ----------------------------------------------------------------------------
+
+
+def soft_threshold(v, t):
+    """S_t(v) = sign(v) max(|v|-t, 0): the closed form of Sec. 4.1 [PAPER.md:384]."""
+    v = np.asarray(v, float)
+    return np.sign(v) * np.maximum(np.abs(v) - t, 0.0)
+
+
+def scalar_subproblem_argmin(g, y, tau, lam, lo, hi):
+    """argmin_{t in [lo,hi]} g*(t-y) + tau/2*(t-y)^2 + lam*|t|   (elementwise).
+
+    Step 1: the unconstrained minimiser of this strongly convex 1-D function is
+    the soft-threshold S_{lam/tau}(y - g/tau).  Step 2: a 1-D convex function
+    restricted to an interval is minimised at the projection of its
+    unconstrained minimiser onto the interval."""
+    u = soft_threshold(y - g / tau, lam / tau)
+    return np.minimum(np.maximum(u, lo), hi)
+
+
+def best_response(P, i: int, xt: np.ndarray, grad: Optional[np.ndarray] = None) -> np.ndarray:
+    """hat x_i(xt), Eq. (2), with the proximal-linear surrogate (module docstring)
+    and, for the DC regularizers, the linearised h^- of Eq. (13) [PAPER.md:534-541]:
+    the smooth gradient is shifted by -lam*grad h^-(xt_i) and the convex part is
+    lam*eta*|x_i|.  ``grad`` (optional) is grad f(xt) restricted to block i."""
+    j0, j1 = P.block_range(i)
+    if grad is None:
+        grad = smooth_grad(P, xt)[j0:j1]
+    y = xt[j0:j1]
+    lo, hi = lo_hi(P)
+    gshift = grad - P.lam * grad_h_minus(P, y)
+    return scalar_subproblem_argmin(gshift, y, P.tau[j0:j1], P.lam * eta(P),
+                                    lo[j0:j1], hi[j0:j1])
+
+
+# ----------------------------------------------------------------------------
+# stationarity measure M_F, Eq. (5) [PAPER.md:287-290]
+# ----------------------------------------------------------------------------
+
+
+def stationarity(P, x: np.ndarray) -> np.ndarray:
+    """M_F(x) = x - argmin_{y in X} {grad f(x)^T (y-x) + g(y) + 1/2||y-x||^2}.
+    For the DC regularizers, f carries -lam*h^- and g = lam*eta|.| (the f/G
+    split of Sec. 4.3 [PAPER.md:533])."""
+    lo, hi = lo_hi(P)
+    g = smooth_grad(P, x) - P.lam * grad_h_minus(P, x)
+    y = scalar_subproblem_argmin(g, x, 1.0, P.lam * eta(P), lo, hi)
+    return x - y
+
+
+def merit_inf(P, x: np.ndarray) -> float:
+    """||hat x(x) - x||_inf, the Sec. 4.3 distance to stationarity [PAPER.md:549]."""
+    g = smooth_grad(P, x)
+    out = 0.0
+    for i in range(P.nblocks):
+        j0, j1 = P.block_range(i)
+        out = max(out, float(np.max(np.abs(best_response(P, i, x, g[j0:j1]) - x[j0:j1]))))
+    return out
+
+
+# ----------------------------------------------------------------------------
+# schedules (S.1) [PAPER.md:253]
+# ----------------------------------------------------------------------------
+
+
+def cyclic_schedule(nblocks: int, sweeps: int) -> Iterable[int]:
+    for _ in range(sweeps):
+        yield from range(nblocks)
+
+
+# ----------------------------------------------------------------------------
+# Algorithm 1 with d^k = 0 (sequential), [PAPER.md:246-260]
+# ----------------------------------------------------------------------------
+
+
+def run_sequential(P, gamma: float, schedule: Iterable[int], x0: Optional[np.ndarray] = None,
+                   refresh_every: int = 0, record_every: int = 0):
+    """Algorithm 1 executed by one core (all delays d^k = 0): for each drawn
+    block i: (S.2) hat x_i(x^k), (S.3) read x_i^k, (S.4)
+    x_i^{k+1} = x_i^k + gamma (hat x_i - x_i^k).
+
+    grad_i f(x^k) = A_i^T phi'(A x^k) is evaluated from z = A x^k.  z is carried
+    forward by the identity A x^{k+1} = A x^k + A_i (x_i^{k+1} - x_i^k)
+    (x changes only in block i); ``refresh_every=1`` recomputes z = A x from
+    scratch at every iteration (the plain definition; the pins compare both).
+    Returns (x, history) with history = [(k, F(x^k))] every ``record_every`` updates."""
+    A = design(P)
+    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    z = A @ x
+    lo, hi = lo_hi(P)
+    hist = []
+    for k, i in enumerate(schedule):
+        if refresh_every and k % refresh_every == 0:
+            z = A @ x
+        j0, j1 = P.block_range(i)
+        Ai = columns(P, j0, j1)
+        if P.loss == "ls":
+            w = 2.0 * P.scale * (z - P.b)
+        else:
+            w = -(P.b / P.m) * expit(-P.b * z)
+        grad = Ai.T @ w - 2.0 * P.c * x[j0:j1]
+        xhat = best_response(P, i, x, grad)
+        xnew = x[j0:j1] + gamma * (xhat - x[j0:j1])
+        z = z + Ai @ (xnew - x[j0:j1])
+        x[j0:j1] = xnew
+        if record_every and (k + 1) % record_every == 0:
+            hist.append((k + 1, objective(P, x)))
+    return x, hist
+
+
+# ----------------------------------------------------------------------------
+# synchronous version (Corollary, x^{k-d} = x^k) [PAPER.md:346-357], Jacobi form
+# ----------------------------------------------------------------------------
+
+
+def jacobi_step(P, x: np.ndarray, gamma: float) -> np.ndarray:
+    """All blocks updated simultaneously from the same x (the synchronous
+    scheme used to estimate F* [PAPER.md:434]): x+ = x + gamma (hat x(x) - x)."""
+    g = smooth_grad(P, x)
+    xnew = x.copy()
+    for i in range(P.nblocks):
+        j0, j1 = P.block_range(i)
+        xhat = best_response(P, i, x, g[j0:j1])
+        xnew[j0:j1] = x[j0:j1] + gamma * (xhat - x[j0:j1])
+    return xnew
+
+
+def run_jacobi(P, gamma: float, sweeps: int, x0: Optional[np.ndarray] = None,
+               keep_iterates: bool = False):
+    """Returns (x, F history [F(x^1)..F(x^T)], iterates or None)."""
+    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    Fs, xs = [], []
+    for _ in range(sweeps):
+        x = jacobi_step(P, x, gamma)
+        Fs.append(objective(P, x))
+        if keep_iterates:
+            xs.append(x.copy())
+    return x, np.array(Fs), (xs if keep_iterates else None)
+
+
+def estimate_fstar(P, gamma: float, max_sweeps: int = 20000, tol: float = 1e-15,
+                   x0: Optional[np.ndarray] = None):
+    """F* estimate: run the sequential (cyclic) scheme "until variations in the
+    objective value were undetectable" [PAPER.md:434]."""
+    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    Fprev = objective(P, x)
+    for s in range(max_sweeps):
+        x, _ = run_sequential(P, gamma, range(P.nblocks), x0=x)
+        F = objective(P, x)
+        if abs(Fprev - F) <= tol * max(1.0, abs(F)):
+            return x, F, s + 1
+        Fprev = F
+    return x, F, max_sweeps
+
+
+def relative_error(Fx: float, Fstar: float) -> float:
+    """(F(x) - F*)/|F*| -- the 'relative error on the objective' of Sec. 4.2 [PAPER.md:451]."""
+    return (Fx - Fstar) / abs(Fstar)
