@@ -214,6 +214,72 @@ def cyclic_schedule(nblocks: int, sweeps: int) -> Iterable[int]:
         yield from range(nblocks)
 
 
+M32 = 0xFFFFFFFF
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), written out in Python.
+    Pinned by the Random123 known-answer vectors in the tests."""
+    c0, c1, c2, c3 = (int(v) & M32 for v in ctr)
+    k0, k1 = (int(v) & M32 for v in key)
+    for i in range(10):
+        if i > 0:
+            k0 = (k0 + 0x9E3779B9) & M32
+            k1 = (k1 + 0xBB67AE85) & M32
+        p0 = 0xD2511F53 * c0
+        p1 = 0xCD9E8D57 * c2
+        hi0, lo0 = p0 >> 32, p0 & M32
+        hi1, lo1 = p1 >> 32, p1 & M32
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+    return [c0, c1, c2, c3]
+
+
+def _fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & M32
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & M32
+    h ^= h >> 16
+    return h
+
+
+def random_epoch_order(seed: int, epoch: int, nblocks: int) -> list:
+    """The random schedule of one epoch (reading R6): the permutation
+    i -> pi_e(i) of the N blocks given by a 4-round Feistel network on [0, 2^d)
+    (d even, 2^d >= N) keyed by one Philox4x32-10 draw at counter
+    (epoch_lo, epoch_hi, 0x5EED, 0xA5F1) with key (seed_lo, seed_hi), and
+    cycle-walking back into [0, N)."""
+    keys = philox4x32_10([epoch & M32, (epoch >> 32) & M32, 0x5EED, 0xA5F1],
+                         [seed & M32, (seed >> 32) & M32])
+    d = 2
+    while (1 << d) < nblocks:
+        d += 1
+    if d & 1:
+        d += 1
+    half = d // 2
+    mask = (1 << half) - 1
+
+    def enc(v):
+        L, R = v >> half, v & mask
+        for r in range(4):
+            F = _fmix32((R & M32) ^ keys[r] ^ (R >> 32)) & mask
+            L, R = R, L ^ F
+        return (L << half) | R
+
+    out = []
+    for i in range(nblocks):
+        v = enc(i)
+        while v >= nblocks:
+            v = enc(v)
+        out.append(v)
+    return out
+
+
+def random_schedule(seed: int, nblocks: int, sweeps: int, epoch0: int = 0) -> Iterable[int]:
+    for e in range(epoch0, epoch0 + sweeps):
+        yield from random_epoch_order(seed, e, nblocks)
+
+
 # ----------------------------------------------------------------------------
 # Algorithm 1 with d^k = 0 (sequential), [PAPER.md:246-260]
 # ----------------------------------------------------------------------------

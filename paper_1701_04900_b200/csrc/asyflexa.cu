@@ -1,0 +1,745 @@
+// asyflexa.cu -- host runtime behind the C ABI of include/asyflexa.h.
+//
+// Owns device memory, validates the problem statement (problem (1)
+// [PAPER.md:58-68]), launches the kernels of dense_async.cuh,
+// sparse_async.cuh and sync_kernels.cuh on the handle's stream, and times the
+// update kernels with CUDA events on that stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "../../include/asyflexa.h"
+#include "common.cuh"
+#include "dense_async.cuh"
+#include "sparse_async.cuh"
+#include "sync_kernels.cuh"
+
+using namespace asy;
+
+static std::string g_create_error;
+
+struct Dev {
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool own = false;
+};
+
+struct asy_handle {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    // problem
+    bool has_problem = false;
+    int kind = 0, loss = 0, reg = 0;
+    int64_t m = 0, n = 0, lda = 0, nnz = 0, B = 1, nblk = 0;
+    Scalars S{};
+    Dev A, colptr, rowidx, vals;          // borrowed or owned
+    Dev rowptr, csr_col, csr_val;         // CSR transpose (owned)
+    Dev b, tau, lo, hi;                   // owned copies
+    // state
+    Dev x, r, dx, w, mf, mer, rs, xs;     // rs/xs: scratch residual / iterate for stationarity
+    Dev part;                             // GEMV-N partial sums
+    int64_t gemv_chunks = 1, gemv_cpc = 1;
+    Dev red_part, red_out;                // reduction buffers
+    // async state
+    Dev counter, gacc, dxr, dpart, arrive, consumed, ready, done, ver;
+    int64_t slots = 0;
+    int64_t epochs = 0;                   // sweeps since reset (schedule epoch)
+
+    int fail(int code, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return code;
+    }
+};
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return h->fail(ASY_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),   \
+                           __FILE__, __LINE__);                                                   \
+    } while (0)
+#define CKL()                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = cudaGetLastError();                                                      \
+        if (e_ != cudaSuccess)                                                                    \
+            return h->fail(ASY_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                           __FILE__, __LINE__);                                                   \
+    } while (0)
+#define TRY(expr)                  \
+    do {                           \
+        int rc_ = (expr);          \
+        if (rc_ != ASY_OK) return rc_; \
+    } while (0)
+
+static void dev_free(Dev& d) {
+    if (d.own && d.p) cudaFree(d.p);
+    d = Dev{};
+}
+
+static int dev_alloc(asy_handle* h, Dev& d, size_t bytes) {
+    if (d.own && d.bytes >= bytes && d.p) return ASY_OK;
+    dev_free(d);
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&d.p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        d = Dev{};
+        return h->fail(ASY_ERR_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    d.bytes = bytes;
+    d.own = true;
+    return ASY_OK;
+}
+
+template <typename T>
+static T* P_(Dev& d) { return reinterpret_cast<T*>(d.p); }
+
+static int copy_in(asy_handle* h, Dev& d, const void* src, size_t bytes, int mem) {
+    TRY(dev_alloc(h, d, bytes));
+    CK(cudaMemcpyAsync(d.p, src, bytes, mem == ASY_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       h->stream));
+    return ASY_OK;
+}
+
+static inline int grid_for(int64_t n, int threads, int cap) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+static int64_t next_pow2(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+static void free_all(asy_handle* h) {
+    Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
+                  &h->tau, &h->lo, &h->hi, &h->x, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
+                  &h->part, &h->red_part, &h->red_out, &h->counter, &h->gacc, &h->dxr, &h->dpart,
+                  &h->arrive, &h->consumed, &h->ready, &h->done, &h->ver};
+    for (Dev* d : all) dev_free(*d);
+    h->has_problem = false;
+}
+
+// --------------------------------------------------------------------------
+// device building blocks
+// --------------------------------------------------------------------------
+
+// out = A v (+ base per mode), deterministic.  Dense: split partial + combine; CSC: CSR rows.
+static int gemvN(asy_handle* h, const double* v, int mode, double* out) {
+    if (h->kind == ASY_DENSE_COLMAJOR) {
+        dim3 grid((unsigned)((h->m + 255) / 256), (unsigned)h->gemv_chunks);
+        dense_gemvN_partial_kernel<<<grid, 256, 0, h->stream>>>(P_<double>(h->A), h->lda, h->m, h->n, v,
+                                                                h->gemv_cpc, P_<double>(h->part));
+        CKL();
+        combine_kernel<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(
+            P_<double>(h->part), h->gemv_chunks, h->m, mode, P_<double>(h->b), out);
+        CKL();
+    } else {
+        csr_gemvN_kernel<<<grid_for(h->m * 8, 256, 8 * h->sms), 256, 0, h->stream>>>(
+            P_<int64_t>(h->rowptr), P_<int32_t>(h->csr_col), P_<double>(h->csr_val), h->m, v, mode,
+            P_<double>(h->b), out);
+        CKL();
+    }
+    return ASY_OK;
+}
+
+// g = A^T w with the per-coordinate epilogue (Jacobi update or stationarity terms).
+static int gemvT(asy_handle* h, const double* w, int mode, double* x, double gamma, double* dx,
+                 double* mf, double* mer) {
+    if (h->kind == ASY_DENSE_COLMAJOR) {
+        dense_gemvT_kernel<<<grid_for(h->n * 32, 256, 16 * h->sms), 256, 0, h->stream>>>(
+            P_<double>(h->A), h->lda, h->m, h->n, w, h->S, mode, x, P_<double>(h->tau), gamma, dx, mf, mer);
+    } else {
+        csc_gemvT_kernel<<<grid_for(h->n * 8, 256, 16 * h->sms), 256, 0, h->stream>>>(
+            P_<int64_t>(h->colptr), P_<int32_t>(h->rowidx), P_<double>(h->vals), h->n, w, h->S, mode, x,
+            P_<double>(h->tau), gamma, dx, mf, mer);
+    }
+    CKL();
+    return ASY_OK;
+}
+
+// out6 (host) = {sum phi(r), sum x^2, sum h(x), #box violations, sum mf^2, max|mf|}
+static int reduce_objective(asy_handle* h, const double* r, const double* x, const double* mf, double out6[6]) {
+    objective_partial_kernel<<<kRedGrid, kRedThreads, 0, h->stream>>>(h->S, r, P_<double>(h->b), h->m, x, h->n, mf,
+                                                                      P_<double>(h->red_part));
+    CKL();
+    reduce_final_kernel<<<1, 32, 0, h->stream>>>(P_<double>(h->red_part), kRedGrid, 1 << 5, P_<double>(h->red_out));
+    CKL();
+    CK(cudaMemcpyAsync(out6, h->red_out.p, 6 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return ASY_OK;
+}
+
+static double objective_from(const asy_handle* h, const double v[6], double* smooth) {
+    const double f = v[0] - 0.5 * h->S.c2 * v[1];
+    if (smooth) *smooth = f;
+    if (v[3] > 0) return INFINITY;
+    return f + h->S.lam * v[2];
+}
+
+static int reset_state(asy_handle* h, const double* x0, int x_mem) {
+    if (x0) {
+        CK(cudaMemcpyAsync(h->x.p, x0, h->n * sizeof(double),
+                           x_mem == ASY_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        TRY(gemvN(h, P_<double>(h->x), h->loss == ASY_LOSS_LS ? COMBINE_FRESH_LS : COMBINE_FRESH_ZERO,
+                  P_<double>(h->r)));
+    } else {
+        fill_kernel<<<grid_for(h->n, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->x), h->n, 0.0);
+        CKL();
+        fresh_residual_base_kernel<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(
+            P_<double>(h->r), P_<double>(h->b), h->m, h->loss == ASY_LOSS_LS);
+        CKL();
+    }
+    h->epochs = 0;
+    return ASY_OK;
+}
+
+// --------------------------------------------------------------------------
+// C ABI
+// --------------------------------------------------------------------------
+extern "C" {
+
+ASY_API const char* asy_version(void) { return "asyflexa-b200 0.1 (sm_100a)"; }
+
+ASY_API const char* asy_last_error(const asy_handle* h) {
+    return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+ASY_API void asy_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    philox4x32_10(ctr, key, out);
+}
+
+ASY_API int asy_schedule_block(int32_t schedule, uint64_t seed, int64_t nblocks, int64_t k, int64_t* out) {
+    if (!out || nblocks < 1 || k < 0 || (schedule != ASY_SCHED_CYCLIC && schedule != ASY_SCHED_RANDOM))
+        return ASY_ERR_INVALID;
+    *out = schedule_block(schedule, seed, nblocks, k);
+    return ASY_OK;
+}
+
+ASY_API int asy_create(int device, void* stream, asy_handle** out) {
+    if (!out) {
+        g_create_error = "asy_create: out is NULL";
+        return ASY_ERR_INVALID;
+    }
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        g_create_error = std::string("asy_create: no CUDA device: ") + cudaGetErrorString(e);
+        return ASY_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) {
+        g_create_error = "asy_create: device index out of range";
+        return ASY_ERR_INVALID;
+    }
+    asy_handle* h = new asy_handle();
+    h->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        g_create_error = "asy_create: cudaSetDevice failed";
+        delete h;
+        return ASY_ERR_CUDA;
+    }
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major < 10) {
+        g_create_error = "asy_create: needs compute capability 10.x (sm_100a)";
+        delete h;
+        return ASY_ERR_UNSUPPORTED;
+    }
+    h->sms = prop.multiProcessorCount;
+    if (stream) {
+        h->stream = reinterpret_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            g_create_error = "asy_create: stream creation failed";
+            delete h;
+            return ASY_ERR_CUDA;
+        }
+        h->own_stream = true;
+    }
+    for (auto& ev : h->ev) cudaEventCreate(&ev);
+    if (dev_alloc(h, h->red_part, sizeof(double) * kRedGrid * kRedVals) != ASY_OK ||
+        dev_alloc(h, h->red_out, sizeof(double) * 8) != ASY_OK ||
+        dev_alloc(h, h->counter, 64) != ASY_OK) {
+        g_create_error = h->err;
+        free_all(h);
+        delete h;
+        return ASY_ERR_NOMEM;
+    }
+    *out = h;
+    return ASY_OK;
+}
+
+ASY_API int asy_destroy(asy_handle* h) {
+    if (!h) return ASY_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    for (auto& ev : h->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return ASY_OK;
+}
+
+ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!p) return h->fail(ASY_ERR_INVALID, "asy_set_problem: problem is NULL");
+    CK(cudaSetDevice(h->device));
+    if (p->m < 1 || p->n < 1) return h->fail(ASY_ERR_INVALID, "m and n must be >= 1");
+    if (p->mem != ASY_MEM_HOST && p->mem != ASY_MEM_DEVICE) return h->fail(ASY_ERR_INVALID, "bad mem kind");
+    if (p->kind != ASY_DENSE_COLMAJOR && p->kind != ASY_CSC) return h->fail(ASY_ERR_INVALID, "bad matrix kind");
+    if (p->loss != ASY_LOSS_LS && p->loss != ASY_LOSS_LOGISTIC) return h->fail(ASY_ERR_INVALID, "bad loss");
+    if (p->reg != ASY_REG_L1 && p->reg != ASY_REG_EXP && p->reg != ASY_REG_LOG)
+        return h->fail(ASY_ERR_INVALID, "bad regularizer");
+    if (p->loss == ASY_LOSS_LS && !(p->loss_scale > 0)) return h->fail(ASY_ERR_INVALID, "loss_scale must be > 0");
+    if (!(p->c_nonconvex >= 0) || !(p->lambda >= 0)) return h->fail(ASY_ERR_INVALID, "c and lambda must be >= 0");
+    if (p->reg != ASY_REG_L1 && !(p->theta > 0)) return h->fail(ASY_ERR_INVALID, "theta must be > 0");
+    if (p->block_size < 1 || p->block_size > 128) return h->fail(ASY_ERR_INVALID, "block_size must be in [1,128]");
+    if (!p->b || !p->tau) return h->fail(ASY_ERR_INVALID, "b and tau are required");
+    if (!p->lo && !p->hi && !(p->lo_all <= p->hi_all)) return h->fail(ASY_ERR_INVALID, "lo_all > hi_all");
+    if ((p->lo == nullptr) != (p->hi == nullptr)) return h->fail(ASY_ERR_INVALID, "lo and hi must both be set or both NULL");
+    if (p->kind == ASY_DENSE_COLMAJOR) {
+        if (!p->A) return h->fail(ASY_ERR_INVALID, "A is NULL");
+        if (p->lda < p->m) return h->fail(ASY_ERR_INVALID, "lda < m");
+    } else {
+        if (!p->colptr || !p->rowidx || !p->vals) return h->fail(ASY_ERR_INVALID, "CSC arrays are NULL");
+        if (p->nnz < 0 || p->nnz >= (int64_t)1 << 31) return h->fail(ASY_ERR_INVALID, "nnz out of range");
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    free_all(h);
+    const int cm = p->mem;
+    h->kind = p->kind;
+    h->loss = p->loss;
+    h->reg = p->reg;
+    h->m = p->m;
+    h->n = p->n;
+    h->B = p->block_size;
+    h->nblk = (p->n + p->block_size - 1) / p->block_size;
+
+    // ---- matrix
+    if (p->kind == ASY_DENSE_COLMAJOR) {
+        const bool aligned = (reinterpret_cast<uintptr_t>(p->A) % 16) == 0 && (p->lda % 2) == 0;
+        if (cm == ASY_MEM_DEVICE && aligned) {
+            h->A.p = const_cast<double*>(p->A);
+            h->A.own = false;
+            h->lda = p->lda;
+        } else {
+            h->lda = (p->m + 15) / 16 * 16;
+            TRY(dev_alloc(h, h->A, sizeof(double) * h->lda * p->n));
+            if (h->lda != p->m) CK(cudaMemsetAsync(h->A.p, 0, sizeof(double) * h->lda * p->n, h->stream));
+            CK(cudaMemcpy2DAsync(h->A.p, sizeof(double) * h->lda, p->A, sizeof(double) * p->lda,
+                                 sizeof(double) * p->m, p->n,
+                                 cm == ASY_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+        }
+        // GEMV-N split: ~4 waves of 256-row tiles over the SMs
+        const int64_t tiles = (h->m + 255) / 256;
+        int64_t chunks = std::max<int64_t>(1, (4 * h->sms + tiles - 1) / tiles);
+        chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, h->n / 8));
+        h->gemv_cpc = (h->n + chunks - 1) / chunks;
+        h->gemv_chunks = (h->n + h->gemv_cpc - 1) / h->gemv_cpc;
+        TRY(dev_alloc(h, h->part, sizeof(double) * h->gemv_chunks * h->m));
+    } else {
+        h->nnz = p->nnz;
+        if (cm == ASY_MEM_DEVICE) {
+            h->colptr.p = const_cast<int64_t*>(p->colptr);
+            h->rowidx.p = const_cast<int32_t*>(p->rowidx);
+            h->vals.p = const_cast<double*>(p->vals);
+        } else {
+            TRY(copy_in(h, h->colptr, p->colptr, sizeof(int64_t) * (p->n + 1), cm));
+            TRY(copy_in(h, h->rowidx, p->rowidx, sizeof(int32_t) * std::max<int64_t>(1, p->nnz), cm));
+            TRY(copy_in(h, h->vals, p->vals, sizeof(double) * std::max<int64_t>(1, p->nnz), cm));
+        }
+        // check colptr ends
+        int64_t ends[2];
+        CK(cudaMemcpyAsync(&ends[0], P_<int64_t>(h->colptr), sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(&ends[1], P_<int64_t>(h->colptr) + p->n, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (ends[0] != 0 || ends[1] != p->nnz) {
+            free_all(h);
+            return h->fail(ASY_ERR_INVALID, "colptr[0] must be 0 and colptr[n] == nnz");
+        }
+        // CSR transpose (deterministic: stable radix sort of row keys over column-major order)
+        const int64_t nnz = std::max<int64_t>(1, p->nnz);
+        Dev colid, perm, keys_out, counts;
+        TRY(dev_alloc(h, colid, sizeof(int32_t) * nnz));
+        TRY(dev_alloc(h, perm, sizeof(int32_t) * nnz));
+        TRY(dev_alloc(h, keys_out, sizeof(int32_t) * nnz));
+        TRY(dev_alloc(h, counts, sizeof(int64_t) * (p->m + 1)));
+        TRY(dev_alloc(h, h->rowptr, sizeof(int64_t) * (p->m + 1)));
+        TRY(dev_alloc(h, h->csr_col, sizeof(int32_t) * nnz));
+        TRY(dev_alloc(h, h->csr_val, sizeof(double) * nnz));
+        Dev iota, bad;
+        TRY(dev_alloc(h, iota, sizeof(int32_t) * nnz));
+        TRY(dev_alloc(h, bad, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(counts.p, 0, sizeof(int64_t) * (p->m + 1), h->stream));
+        if (p->nnz > 0) {
+            expand_colids_kernel<<<grid_for(p->n, 256, 8 * h->sms), 256, 0, h->stream>>>(P_<int64_t>(h->colptr), p->n,
+                                                                                          P_<int32_t>(colid));
+            CKL();
+            iota_kernel<<<grid_for(p->nnz, 256, 8 * h->sms), 256, 0, h->stream>>>(P_<int32_t>(iota), p->nnz);
+            CKL();
+            row_count_kernel<<<grid_for(p->nnz, 256, 8 * h->sms), 256, 0, h->stream>>>(
+                P_<int32_t>(h->rowidx), p->nnz, p->m, P_<int64_t>(counts), P_<unsigned long long>(bad));
+            CKL();
+            size_t tmp_bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, P_<int32_t>(h->rowidx), P_<int32_t>(keys_out),
+                                            P_<int32_t>(iota), P_<int32_t>(perm), (int)p->nnz, 0, 32, h->stream);
+            Dev tmp;
+            TRY(dev_alloc(h, tmp, tmp_bytes));
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, P_<int32_t>(h->rowidx), P_<int32_t>(keys_out),
+                                               P_<int32_t>(iota), P_<int32_t>(perm), (int)p->nnz, 0, 32, h->stream));
+            csr_gather_kernel<<<grid_for(p->nnz, 256, 8 * h->sms), 256, 0, h->stream>>>(
+                P_<int32_t>(perm), P_<int32_t>(colid), P_<double>(h->vals), p->nnz, P_<int32_t>(h->csr_col),
+                P_<double>(h->csr_val));
+            CKL();
+            CK(cudaStreamSynchronize(h->stream));
+            dev_free(tmp);
+        }
+        size_t scan_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, P_<int64_t>(counts), P_<int64_t>(h->rowptr),
+                                      (int)(p->m + 1), h->stream);
+        Dev scan_tmp;
+        TRY(dev_alloc(h, scan_tmp, scan_bytes));
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, P_<int64_t>(counts), P_<int64_t>(h->rowptr),
+                                         (int)(p->m + 1), h->stream));
+        unsigned long long nbad = 0;
+        CK(cudaMemcpyAsync(&nbad, bad.p, sizeof nbad, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        Dev* tmps[] = {&colid, &perm, &keys_out, &counts, &iota, &bad, &scan_tmp};
+        for (Dev* d : tmps) dev_free(*d);
+        if (nbad) {
+            free_all(h);
+            return h->fail(ASY_ERR_INVALID, "rowidx has %llu entries outside [0, m)", nbad);
+        }
+    }
+
+    // ---- vectors
+    TRY(copy_in(h, h->b, p->b, sizeof(double) * p->m, cm));
+    TRY(copy_in(h, h->tau, p->tau, sizeof(double) * p->n, cm));
+    if (p->lo) {
+        TRY(copy_in(h, h->lo, p->lo, sizeof(double) * p->n, cm));
+        TRY(copy_in(h, h->hi, p->hi, sizeof(double) * p->n, cm));
+    }
+    // validate tau / box
+    {
+        Dev bad;
+        TRY(dev_alloc(h, bad, sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), h->stream));
+        validate_kernel<<<grid_for(p->n, 256, 4 * h->sms), 256, 0, h->stream>>>(
+            P_<double>(h->tau), p->lo ? P_<double>(h->lo) : nullptr, p->hi ? P_<double>(h->hi) : nullptr, p->n,
+            P_<unsigned long long>(bad));
+        CKL();
+        unsigned long long nbad = 0;
+        CK(cudaMemcpyAsync(&nbad, bad.p, sizeof nbad, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        dev_free(bad);
+        if (nbad) {
+            free_all(h);
+            return h->fail(ASY_ERR_INVALID, "%llu coordinates with tau <= 0 (or inf/nan) or lo > hi", nbad);
+        }
+    }
+
+    // ---- scalars
+    Scalars& S = h->S;
+    S = Scalars{};
+    S.loss = p->loss;
+    S.reg = p->reg;
+    S.s2 = 2.0 * p->loss_scale;
+    S.minv = 1.0 / (double)p->m;
+    S.c2 = 2.0 * p->c_nonconvex;
+    S.lam = p->lambda;
+    S.theta = p->theta;
+    if (p->reg == ASY_REG_EXP) S.eta = p->theta;
+    else if (p->reg == ASY_REG_LOG) S.eta = p->theta / log1p(p->theta);
+    else S.eta = 1.0;
+    S.inv_log1p_theta = p->reg == ASY_REG_LOG ? 1.0 / log1p(p->theta) : 0.0;
+    S.lam_eff = p->reg == ASY_REG_L1 ? p->lambda : p->lambda * S.eta;
+    S.lo_all = p->lo_all;
+    S.hi_all = p->hi_all;
+    S.lo = p->lo ? P_<double>(h->lo) : nullptr;
+    S.hi = p->hi ? P_<double>(h->hi) : nullptr;
+
+    // ---- state
+    TRY(dev_alloc(h, h->x, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->xs, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->dx, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->mf, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->mer, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->r, sizeof(double) * h->m));
+    TRY(dev_alloc(h, h->rs, sizeof(double) * h->m));
+    TRY(dev_alloc(h, h->w, sizeof(double) * (h->m + 2)));
+    h->has_problem = true;
+    TRY(reset_state(h, nullptr, ASY_MEM_DEVICE));
+    CK(cudaStreamSynchronize(h->stream));
+    return ASY_OK;
+}
+
+// ---- one synchronous Jacobi sweep
+static int jacobi_sweep(asy_handle* h, double gamma) {
+    loss_weights_kernel<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(h->S, P_<double>(h->r),
+                                                                                  P_<double>(h->b), P_<double>(h->w), h->m);
+    CKL();
+    TRY(gemvT(h, P_<double>(h->w), GT_JACOBI, P_<double>(h->x), gamma, P_<double>(h->dx), nullptr, nullptr));
+    TRY(gemvN(h, P_<double>(h->dx), COMBINE_ADD, P_<double>(h->r)));
+    return ASY_OK;
+}
+
+// ---- async launches
+static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
+                              float* ms) {
+    const int64_t B = h->B;
+    int64_t R = sp->panel_rows;
+    if (R <= 0) {
+        R = 4096 / B;
+        R = std::max<int64_t>(16, std::min<int64_t>(R, 2048));
+    }
+    R &= ~1ll;
+    if (R < 2) R = 2;
+    const int64_t mEven = (h->m + 1) & ~1ll;
+    if (R > mEven) R = mEven;
+    const int64_t G = (h->m + R - 1) / R;
+    const int Bmax = (int)B;
+    const size_t panel_bytes = sizeof(double) * R * Bmax;
+    const size_t fixed = sizeof(double) * (R + Bmax) + 8 * sizeof(long long) * 0;
+    int NS = sp->stages;
+    if (NS <= 0) {
+        NS = (int)std::min<int64_t>(8, std::max<int64_t>(2, (int64_t)((200 * 1024 - fixed) / panel_bytes)));
+    }
+    const size_t smem = panel_bytes * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t)) + 64;
+    if (smem > 227 * 1024)
+        return h->fail(ASY_ERR_INVALID, "panel_rows*block_size*stages too large for shared memory (%zu B)", smem);
+    CK(cudaFuncSetAttribute(dense_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_async_kernel, kDenseThreads, smem));
+    if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense async kernel does not fit on an SM");
+    int grid = occ * h->sms;
+    if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
+
+    const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * slots * Bmax));
+    TRY(dev_alloc(h, h->dxr, sizeof(double) * slots * Bmax));
+    TRY(dev_alloc(h, h->dpart, sizeof(double) * G * Bmax));
+    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
+    TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots));
+    TRY(dev_alloc(h, h->ready, sizeof(long long) * slots));
+    TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
+    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk * G));
+
+    DenseAsyncParams P{};
+    P.A = P_<double>(h->A);
+    P.lda = h->lda; P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
+    P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x); P.tau = P_<double>(h->tau);
+    P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
+    P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
+    P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc); P.dxr = P_<double>(h->dxr);
+    P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
+    P.ready = P_<long long>(h->ready); P.done = P_<long long>(h->done); P.ver = P_<unsigned>(h->ver);
+    P.slots = slots; P.Bmax = Bmax; P.stages = NS;
+
+    dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk * G), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    CKL();
+    void* args[] = {&P};
+    CK(cudaEventRecord(h->ev[0], h->stream));
+    CK(cudaLaunchCooperativeKernel((void*)dense_async_kernel, dim3(grid), dim3(kDenseThreads), args, smem, h->stream));
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventSynchronize(h->ev[1]));
+    CKL();
+    CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    return ASY_OK;
+}
+
+static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
+                               float* ms) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_async_kernel, 256, 0));
+    int grid = std::max(1, occ) * h->sms;
+    if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
+    const int64_t slots = next_pow2(std::max<int64_t>(1 << 20, 2 * (delay + 2)));
+    TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
+    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->n));
+    SparseAsyncParams P{};
+    P.colptr = P_<int64_t>(h->colptr); P.rowidx = P_<int32_t>(h->rowidx); P.vals = P_<double>(h->vals);
+    P.m = h->m; P.n = h->n; P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x);
+    P.tau = P_<double>(h->tau); P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed;
+    P.epoch0 = h->epochs; P.K = sweeps * h->n; P.delay = delay; P.counter = P_<unsigned long long>(h->counter);
+    P.ver = P_<unsigned>(h->ver); P.done = P_<long long>(h->done); P.slots = slots;
+    P.chunk = delay == 0 ? 4 : 32;
+    sparse_async_init<<<grid_for(std::max<int64_t>(slots, h->n), 256, 8 * h->sms), 256, 0, h->stream>>>(P);
+    CKL();
+    void* args[] = {&P};
+    CK(cudaEventRecord(h->ev[0], h->stream));
+    CK(cudaLaunchCooperativeKernel((void*)sparse_async_kernel, dim3(grid), dim3(256), args, 0, h->stream));
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventSynchronize(h->ev[1]));
+    CKL();
+    CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    return ASY_OK;
+}
+
+ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats* st) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!sp) return h->fail(ASY_ERR_INVALID, "asy_solve: params NULL");
+    if (!h->has_problem) return h->fail(ASY_ERR_STATE, "asy_solve before asy_set_problem");
+    if (!(sp->gamma > 0 && sp->gamma <= 1)) return h->fail(ASY_ERR_INVALID, "gamma must be in (0, 1]");
+    if (sp->sweeps < 0) return h->fail(ASY_ERR_INVALID, "sweeps < 0");
+    if (sp->mode != ASY_MODE_ASYNC && sp->mode != ASY_MODE_SYNC_JACOBI) return h->fail(ASY_ERR_INVALID, "bad mode");
+    if (sp->schedule != ASY_SCHED_CYCLIC && sp->schedule != ASY_SCHED_RANDOM)
+        return h->fail(ASY_ERR_INVALID, "bad schedule");
+    if (sp->x_mem != ASY_MEM_HOST && sp->x_mem != ASY_MEM_DEVICE) return h->fail(ASY_ERR_INVALID, "bad x_mem");
+    if (sp->panel_rows < 0 || (sp->panel_rows & 1)) return h->fail(ASY_ERR_INVALID, "panel_rows must be even");
+    if (sp->stages < 0 || sp->stages > 16) return h->fail(ASY_ERR_INVALID, "stages must be in [0,16]");
+    CK(cudaSetDevice(h->device));
+    asy_solve_stats stats{};
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    if (sp->reset) TRY(reset_state(h, sp->x0, sp->x_mem));
+    int64_t delay = sp->max_delay;
+    if (delay < 0) delay = std::max<int64_t>(1, h->nblk / 8);
+    delay = std::min<int64_t>(delay, 1 << 22);
+    double kernel_ms = 0;
+    int64_t launches = sp->reset ? 2 : 0;
+    for (int64_t done = 0; done < sp->sweeps;) {
+        const int64_t chunk = sp->f_hist ? 1 : sp->sweeps;
+        if (sp->mode == ASY_MODE_SYNC_JACOBI) {
+            cudaEventRecord(h->ev[0], h->stream);
+            for (int64_t s = 0; s < chunk; ++s) TRY(jacobi_sweep(h, sp->gamma));
+            cudaEventRecord(h->ev[1], h->stream);
+            CK(cudaEventSynchronize(h->ev[1]));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+            kernel_ms += ms;
+            launches += chunk * (h->kind == ASY_DENSE_COLMAJOR ? 4 : 3);
+        } else {
+            float ms = 0;
+            if (h->kind == ASY_DENSE_COLMAJOR) TRY(dense_async_launch(h, sp, chunk, delay, &ms));
+            else TRY(sparse_async_launch(h, sp, chunk, delay, &ms));
+            kernel_ms += ms;
+            launches += 2;
+        }
+        h->epochs += chunk;
+        stats.block_updates += chunk * (sp->mode == ASY_MODE_SYNC_JACOBI ? h->nblk : h->nblk);
+        if (sp->f_hist) {
+            double v[6];
+            TRY(reduce_objective(h, P_<double>(h->r), P_<double>(h->x), nullptr, v));
+            sp->f_hist[done] = objective_from(h, v, nullptr);
+            launches += 2;
+        }
+        done += chunk;
+    }
+    {
+        double v[6];
+        TRY(reduce_objective(h, P_<double>(h->r), P_<double>(h->x), nullptr, v));
+        stats.objective = objective_from(h, v, nullptr);
+        launches += 2;
+    }
+    if (sp->x_out)
+        CK(cudaMemcpyAsync(sp->x_out, h->x.p, sizeof(double) * h->n,
+                           sp->x_mem == ASY_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaEventRecord(h->ev[3], h->stream));
+    CK(cudaEventSynchronize(h->ev[3]));
+    float tot = 0;
+    cudaEventElapsedTime(&tot, h->ev[2], h->ev[3]);
+    stats.kernel_ms = kernel_ms;
+    stats.total_ms = tot;
+    stats.launches = launches;
+    stats.epochs = h->epochs;
+    if (st) *st = stats;
+    return ASY_OK;
+}
+
+ASY_API int asy_stationarity(asy_handle* h, const double* x, int32_t x_mem, asy_stationarity_out* out) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!out) return h->fail(ASY_ERR_INVALID, "out is NULL");
+    if (!h->has_problem) return h->fail(ASY_ERR_STATE, "no problem set");
+    if (x && x_mem != ASY_MEM_HOST && x_mem != ASY_MEM_DEVICE) return h->fail(ASY_ERR_INVALID, "bad x_mem");
+    CK(cudaSetDevice(h->device));
+    double* xs = P_<double>(h->xs);
+    CK(cudaMemcpyAsync(xs, x ? x : h->x.p, sizeof(double) * h->n,
+                       (x && x_mem == ASY_MEM_HOST) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+    // fresh residual, weights, gradient + per-coordinate M_F / merit
+    TRY(gemvN(h, xs, h->loss == ASY_LOSS_LS ? COMBINE_FRESH_LS : COMBINE_FRESH_ZERO, P_<double>(h->rs)));
+    loss_weights_kernel<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(h->S, P_<double>(h->rs),
+                                                                                  P_<double>(h->b), P_<double>(h->w), h->m);
+    CKL();
+    TRY(gemvT(h, P_<double>(h->w), GT_STATIONARITY, xs, 0.0, nullptr, P_<double>(h->mf), P_<double>(h->mer)));
+    double v[6];
+    TRY(reduce_objective(h, P_<double>(h->rs), xs, P_<double>(h->mf), v));
+    out->objective = objective_from(h, v, &out->smooth);
+    out->mf_norm2 = sqrt(v[4]);
+    out->mf_norminf = v[5];
+    max_partial_kernel<<<kRedGrid, kRedThreads, 0, h->stream>>>(P_<double>(h->mer), h->n, P_<double>(h->red_part));
+    CKL();
+    reduce_final_kernel<<<1, 32, 0, h->stream>>>(P_<double>(h->red_part), kRedGrid, 0x3F, P_<double>(h->red_out));
+    CKL();
+    double mx[6];
+    CK(cudaMemcpyAsync(mx, h->red_out.p, sizeof mx, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    out->merit_inf = mx[0];
+    return ASY_OK;
+}
+
+ASY_API int asy_get_x(asy_handle* h, double* x, int32_t x_mem) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!x) return h->fail(ASY_ERR_INVALID, "x is NULL");
+    if (!h->has_problem) return h->fail(ASY_ERR_STATE, "no problem set");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(x, h->x.p, sizeof(double) * h->n,
+                       x_mem == ASY_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return ASY_OK;
+}
+
+ASY_API int asy_objective(asy_handle* h, double* F) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!F) return h->fail(ASY_ERR_INVALID, "F is NULL");
+    if (!h->has_problem) return h->fail(ASY_ERR_STATE, "no problem set");
+    CK(cudaSetDevice(h->device));
+    double v[6];
+    TRY(reduce_objective(h, P_<double>(h->r), P_<double>(h->x), nullptr, v));
+    *F = objective_from(h, v, nullptr);
+    return ASY_OK;
+}
+
+ASY_API int asy_schedule_device(asy_handle* h, int32_t schedule, uint64_t seed, int64_t nblocks, int64_t k0,
+                                int64_t count, int64_t* out) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!out || nblocks < 1 || k0 < 0 || count < 0 ||
+        (schedule != ASY_SCHED_CYCLIC && schedule != ASY_SCHED_RANDOM))
+        return h->fail(ASY_ERR_INVALID, "asy_schedule_device: bad arguments");
+    CK(cudaSetDevice(h->device));
+    Dev buf;
+    TRY(dev_alloc(h, buf, sizeof(int64_t) * std::max<int64_t>(1, count)));
+    schedule_kernel<<<grid_for(count, 256, 8 * h->sms), 256, 0, h->stream>>>(schedule, seed, nblocks, k0, count,
+                                                                            P_<int64_t>(buf));
+    CKL();
+    CK(cudaMemcpyAsync(out, buf.p, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    dev_free(buf);
+    return ASY_OK;
+}
+
+}  // extern "C"
