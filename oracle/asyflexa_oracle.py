@@ -51,7 +51,17 @@ def columns(P, j0: int, j1: int):
     """A_i = columns j0..j1-1 of A (dense ndarray)."""
     if P.kind == "dense":
         return P.A[:, j0:j1]
-    return design(P)[:, j0:j1].toarray()
+    out = np.zeros((P.m, j1 - j0))
+    for j in range(j0, j1):
+        s, e = P.colptr[j], P.colptr[j + 1]
+        out[P.rowidx[s:e], j - j0] = P.vals[s:e]
+    return out
+
+
+def default_x0(P) -> np.ndarray:
+    """x^0 in X (Algorithm 1 initialisation [PAPER.md:250]): the projection of 0 onto the box."""
+    lo, hi = lo_hi(P)
+    return np.minimum(np.maximum(np.zeros(P.n), lo), hi)
 
 
 def lo_hi(P):
@@ -297,7 +307,7 @@ def run_sequential(P, gamma: float, schedule: Iterable[int], x0: Optional[np.nda
     scratch at every iteration (the plain definition; the pins compare both).
     Returns (x, history) with history = [(k, F(x^k))] every ``record_every`` updates."""
     A = design(P)
-    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    x = default_x0(P) if x0 is None else np.array(x0, float)
     z = A @ x
     lo, hi = lo_hi(P)
     hist = []
@@ -340,7 +350,7 @@ def jacobi_step(P, x: np.ndarray, gamma: float) -> np.ndarray:
 def run_jacobi(P, gamma: float, sweeps: int, x0: Optional[np.ndarray] = None,
                keep_iterates: bool = False):
     """Returns (x, F history [F(x^1)..F(x^T)], iterates or None)."""
-    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    x = default_x0(P) if x0 is None else np.array(x0, float)
     Fs, xs = [], []
     for _ in range(sweeps):
         x = jacobi_step(P, x, gamma)
@@ -354,7 +364,7 @@ def estimate_fstar(P, gamma: float, max_sweeps: int = 20000, tol: float = 1e-15,
                    x0: Optional[np.ndarray] = None):
     """F* estimate: run the sequential (cyclic) scheme "until variations in the
     objective value were undetectable" [PAPER.md:434]."""
-    x = np.zeros(P.n) if x0 is None else np.array(x0, float)
+    x = default_x0(P) if x0 is None else np.array(x0, float)
     Fprev = objective(P, x)
     for s in range(max_sweeps):
         x, _ = run_sequential(P, gamma, range(P.nblocks), x0=x)

@@ -133,13 +133,21 @@ static int64_t next_pow2(int64_t v) {
     return p;
 }
 
-static void free_all(asy_handle* h) {
+// problem-owned buffers (the handle-lifetime ones -- red_part, red_out, counter -- survive)
+static void free_problem(asy_handle* h) {
     Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
                   &h->tau, &h->lo, &h->hi, &h->x, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
-                  &h->part, &h->red_part, &h->red_out, &h->counter, &h->gacc, &h->dxr, &h->dpart,
-                  &h->arrive, &h->consumed, &h->ready, &h->done, &h->ver};
+                  &h->part, &h->gacc, &h->dxr, &h->dpart, &h->arrive, &h->consumed, &h->ready, &h->done,
+                  &h->ver};
     for (Dev* d : all) dev_free(*d);
     h->has_problem = false;
+}
+
+static void free_all(asy_handle* h) {
+    free_problem(h);
+    dev_free(h->red_part);
+    dev_free(h->red_out);
+    dev_free(h->counter);
 }
 
 // --------------------------------------------------------------------------
@@ -206,11 +214,11 @@ static int reset_state(asy_handle* h, const double* x0, int x_mem) {
         TRY(gemvN(h, P_<double>(h->x), h->loss == ASY_LOSS_LS ? COMBINE_FRESH_LS : COMBINE_FRESH_ZERO,
                   P_<double>(h->r)));
     } else {
-        fill_kernel<<<grid_for(h->n, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->x), h->n, 0.0);
+        // x0 = P_X(0); r = A x0 - b (the GEMV skips the zero columns of x0)
+        project_zero_kernel<<<grid_for(h->n, 256, 4 * h->sms), 256, 0, h->stream>>>(h->S, P_<double>(h->x), h->n);
         CKL();
-        fresh_residual_base_kernel<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(
-            P_<double>(h->r), P_<double>(h->b), h->m, h->loss == ASY_LOSS_LS);
-        CKL();
+        TRY(gemvN(h, P_<double>(h->x), h->loss == ASY_LOSS_LS ? COMBINE_FRESH_LS : COMBINE_FRESH_ZERO,
+                  P_<double>(h->r)));
     }
     h->epochs = 0;
     return ASY_OK;
@@ -330,7 +338,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
         if (p->nnz < 0 || p->nnz >= (int64_t)1 << 31) return h->fail(ASY_ERR_INVALID, "nnz out of range");
     }
     CK(cudaStreamSynchronize(h->stream));
-    free_all(h);
+    free_problem(h);
     const int cm = p->mem;
     h->kind = p->kind;
     h->loss = p->loss;
@@ -379,7 +387,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
         CK(cudaMemcpyAsync(&ends[1], P_<int64_t>(h->colptr) + p->n, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
         if (ends[0] != 0 || ends[1] != p->nnz) {
-            free_all(h);
+            free_problem(h);
             return h->fail(ASY_ERR_INVALID, "colptr[0] must be 0 and colptr[n] == nnz");
         }
         // CSR transpose (deterministic: stable radix sort of row keys over column-major order)
@@ -433,7 +441,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
         Dev* tmps[] = {&colid, &perm, &keys_out, &counts, &iota, &bad, &scan_tmp};
         for (Dev* d : tmps) dev_free(*d);
         if (nbad) {
-            free_all(h);
+            free_problem(h);
             return h->fail(ASY_ERR_INVALID, "rowidx has %llu entries outside [0, m)", nbad);
         }
     }
@@ -459,7 +467,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
         CK(cudaStreamSynchronize(h->stream));
         dev_free(bad);
         if (nbad) {
-            free_all(h);
+            free_problem(h);
             return h->fail(ASY_ERR_INVALID, "%llu coordinates with tau <= 0 (or inf/nan) or lo > hi", nbad);
         }
     }

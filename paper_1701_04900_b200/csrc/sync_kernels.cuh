@@ -237,6 +237,12 @@ __global__ void reduce_final_kernel(const double* __restrict__ partial, int npar
     out[q] = a;
 }
 
+// x0 = projection of 0 onto the box X (Algorithm 1 initialisation, x^0 in X [PAPER.md:250])
+__global__ void project_zero_kernel(Scalars S, double* x, int64_t n) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        x[j] = fmin(fmax(0.0, box_lo(S, j)), box_hi(S, j));
+}
+
 // x <- value / copy helpers
 __global__ void fill_kernel(double* a, int64_t n, double v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

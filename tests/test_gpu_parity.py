@@ -15,6 +15,7 @@ import pytest
 
 from oracle import asyflexa_oracle as O
 from paper_1701_04900_b200 import inputs
+from cases import make_case
 
 pytestmark = pytest.mark.gpu
 
@@ -35,45 +36,6 @@ def _rel_x(a, b):
 
 def _rel_f(a, b):
     return abs(a - b) / max(1.0, abs(b))
-
-
-def make_case(name):
-    if name == "config0":
-        return inputs.config(0)
-    if name == "dense_ragged":   # odd m, ragged last block, several panels
-        return inputs.dense_lasso(203, 517, nnz_frac=0.03, sigma=0.01, lam_frac=0.08, block=32,
-                                  gamma=0.9, seed=5, name="dense_ragged")
-    if name == "dense_normalized":  # config 1 recipe, small
-        return inputs.dense_lasso(400, 800, nnz_frac=0.01, sigma=0.01, lam_frac=0.05, block=32,
-                                  gamma=0.9, normalize=True, seed=2)
-    if name == "nonconvex":       # config 2 recipe, small
-        return inputs.nonconvex_box(60, 130, block=8, gamma=0.5, seed=3, lam_frac=0.3)
-    if name == "large_block":     # config 3 recipe, small, max block size 128
-        return inputs.dense_lasso(300, 700, nnz_frac=0.005, sigma=0.01, lam_frac=0.02, block=128,
-                                  gamma=0.9, seed=4)
-    if name == "sparse_logistic":  # config 4 recipe, small
-        return inputs.sparse_logistic(300, 900, density=0.03, seed=6, lam_frac=0.02)
-    if name == "sparse_ls":
-        P = inputs.sparse_logistic(250, 400, density=0.05, seed=7)
-        A = inputs.csc_to_dense(P)
-        xb = inputs.sparse_signal(7, P.n, 12)
-        b = A @ xb + 0.01 * np.random.default_rng(7).standard_normal(P.m)
-        P.loss, P.scale, P.b = "ls", 0.5, b
-        P.lam = 0.05 * float(np.max(np.abs(A.T @ b)))
-        P.tau = np.maximum(np.sum(A * A, axis=0), 1e-3)
-        return P
-    if name == "dense_logistic":
-        P = inputs.sparse_logistic(180, 240, density=0.2, seed=8, lam_frac=0.02)
-        P.A = inputs.csc_to_dense(P)
-        P.kind, P.block = "dense", 4
-        return P
-    if name in ("dc_exp", "dc_log"):
-        P = inputs.nonconvex_box(80, 120, block=1, gamma=0.9, seed=9, lam_frac=0.05)
-        P.c, P.lo, P.hi = 0.0, -np.inf, np.inf
-        P.reg, P.theta = name[3:], 20.0
-        P.lam = 0.1 * P.lam / 20.0
-        return P
-    raise KeyError(name)
 
 
 SEQ_CASES = ["config0", "dense_ragged", "nonconvex", "large_block", "sparse_logistic", "sparse_ls",
