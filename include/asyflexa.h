@@ -126,7 +126,7 @@ typedef struct {
     double* x_out;         /* n entries or NULL: final x copied here */
     double* f_hist;        /* HOST array of `sweeps` entries or NULL: F(x) after every sweep */
     int32_t workers;       /* async: CTAs (0 = all resident) */
-    int32_t panel_rows;    /* dense async: rows per panel (0 = auto, must be even) */
+    int32_t panel_rows;    /* dense async: rows per panel (0 = auto; multiple of 32, <= 256) */
     int32_t stages;        /* dense async: smem pipeline stages (0 = auto) */
 } asy_solve_params;
 

@@ -518,27 +518,42 @@ static int jacobi_sweep(asy_handle* h, double gamma) {
 }
 
 // ---- async launches
-static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
-                              float* ms) {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+struct DenseGeom {
+    int64_t R, G;
+    int NS, grid;
+    size_t smem;
+};
+
+static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t delay, DenseGeom* g) {
     const int64_t B = h->B;
     int64_t R = sp->panel_rows;
-    if (R <= 0) {
-        R = 4096 / B;
-        R = std::max<int64_t>(16, std::min<int64_t>(R, 2048));
-    }
-    R &= ~1ll;
-    if (R < 2) R = 2;
-    const int64_t mEven = (h->m + 1) & ~1ll;
-    if (R > mEven) R = mEven;
+    if (R <= 0) R = 4096 / B;                       // ~32 KB panels
+    R = (R + 31) / 32 * 32;
+    R = std::max<int64_t>(32, std::min<int64_t>(R, 256));
+    const int64_t mr = (h->m + 31) / 32 * 32;
+    if (R > mr) R = mr;
     const int64_t G = (h->m + R - 1) / R;
-    const int Bmax = (int)B;
-    const size_t panel_bytes = sizeof(double) * R * Bmax;
-    const size_t fixed = sizeof(double) * (R + Bmax) + 8 * sizeof(long long) * 0;
+    const size_t panel = sizeof(double) * R * B;
+    const size_t fixed = sizeof(double) * (kDotWarps * R + kAxpyWarps * B) + 1024;
     int NS = sp->stages;
-    if (NS <= 0) {
-        NS = (int)std::min<int64_t>(8, std::max<int64_t>(2, (int64_t)((200 * 1024 - fixed) / panel_bytes)));
-    }
-    const size_t smem = panel_bytes * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t)) + 64;
+    if (NS <= 0) NS = (int)std::min<int64_t>(16, std::max<int64_t>(2, (int64_t)((220 * 1024 - fixed) / panel)));
+    const size_t smem = panel * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t));
     if (smem > 227 * 1024)
         return h->fail(ASY_ERR_INVALID, "panel_rows*block_size*stages too large for shared memory (%zu B)", smem);
     CK(cudaFuncSetAttribute(dense_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -546,7 +561,31 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_async_kernel, kDenseThreads, smem));
     if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense async kernel does not fit on an SM");
     int grid = occ * h->sms;
+    // enough workers to keep ~2x the delay window of panels in flight, never more
+    const int64_t want = (2 * (delay + 1) * G + NS - 1) / NS;
+    if (want < grid) grid = (int)std::max<int64_t>(1, want);
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
+    g->R = R; g->G = G; g->NS = NS; g->grid = grid; g->smem = smem;
+    return ASY_OK;
+}
+
+static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
+                              float* ms) {
+    DenseGeom geo;
+    TRY(dense_geometry(h, sp, delay, &geo));
+    const int64_t B = h->B, R = geo.R, G = geo.G;
+    const int Bmax = (int)B;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {(cuuint64_t)h->m, (cuuint64_t)h->n};
+    cuuint64_t strides[1] = {(cuuint64_t)(h->lda * sizeof(double))};
+    cuuint32_t box[2] = {(cuuint32_t)R, (cuuint32_t)B};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->A.p, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 
     const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
     TRY(dev_alloc(h, h->gacc, sizeof(double) * slots * Bmax));
@@ -559,21 +598,21 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk * G));
 
     DenseAsyncParams P{};
-    P.A = P_<double>(h->A);
-    P.lda = h->lda; P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
+    P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x); P.tau = P_<double>(h->tau);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
     P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
     P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc); P.dxr = P_<double>(h->dxr);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
     P.ready = P_<long long>(h->ready); P.done = P_<long long>(h->done); P.ver = P_<unsigned>(h->ver);
-    P.slots = slots; P.Bmax = Bmax; P.stages = NS;
+    P.slots = slots; P.Bmax = Bmax; P.stages = geo.NS;
 
     dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk * G), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
-    void* args[] = {&P};
+    void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));
-    CK(cudaLaunchCooperativeKernel((void*)dense_async_kernel, dim3(grid), dim3(kDenseThreads), args, smem, h->stream));
+    CK(cudaLaunchCooperativeKernel((void*)dense_async_kernel, dim3(geo.grid), dim3(kDenseThreads), args, geo.smem,
+                                   h->stream));
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
@@ -619,7 +658,8 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     if (sp->schedule != ASY_SCHED_CYCLIC && sp->schedule != ASY_SCHED_RANDOM)
         return h->fail(ASY_ERR_INVALID, "bad schedule");
     if (sp->x_mem != ASY_MEM_HOST && sp->x_mem != ASY_MEM_DEVICE) return h->fail(ASY_ERR_INVALID, "bad x_mem");
-    if (sp->panel_rows < 0 || (sp->panel_rows & 1)) return h->fail(ASY_ERR_INVALID, "panel_rows must be even");
+    if (sp->panel_rows < 0 || (sp->panel_rows % 32) || sp->panel_rows > 256)
+        return h->fail(ASY_ERR_INVALID, "panel_rows must be a multiple of 32 in [0, 256]");
     if (sp->stages < 0 || sp->stages > 16) return h->fail(ASY_ERR_INVALID, "stages must be in [0,16]");
     CK(cudaSetDevice(h->device));
     asy_solve_stats stats{};

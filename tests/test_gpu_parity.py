@@ -272,7 +272,7 @@ def test_invalid_arguments(A):
     with pytest.raises(A.AsyError):
         S.solve(gamma=1.5)
     with pytest.raises(A.AsyError):
-        S.solve(panel_rows=3)
+        S.solve(panel_rows=48)
     S.close()
     P.block = 0
     with pytest.raises(A.AsyError):
