@@ -311,13 +311,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         __syncwarp();
         const long long r0 = p * R;
         if (nz) {
-            for (int q = 0; q < rows_per_lane; ++q) {
-                const int i = lane + 32 * q;
-                const double* a = pan + i;
-                double d = 0.0;
-                for (int c = 0; c < nc; ++c) d = fma(a[(size_t)c * R], dv[c], d);
-                const long long row = r0 + i;
-                if (row < P.m && d != 0.0) atomicAdd(&P.r[row], d);
+            // rows_per_lane independent FMA chains (one per row), dx broadcast from smem
+            double d[kMaxRowsPerLane];
+#pragma unroll
+            for (int q = 0; q < kMaxRowsPerLane; ++q) d[q] = 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double dc = dv[c];
+                const double* a = pan + (size_t)c * R + lane;
+#pragma unroll
+                for (int q = 0; q < kMaxRowsPerLane; ++q)
+                    if (q < rows_per_lane) d[q] = fma(a[32 * q], dc, d[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                const long long row = r0 + lane + 32 * q;
+                if (q < rows_per_lane && row < P.m && d[q] != 0.0) atomicAdd(&P.r[row], d[q]);
             }
         }
         __syncwarp();
