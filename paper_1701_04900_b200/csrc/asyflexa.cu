@@ -536,23 +536,33 @@ static EncodeTiledFn encode_tiled() {
 
 struct DenseGeom {
     int64_t R, G;
-    int NS, grid;
+    int NS, TS, Bpad, grid;
     size_t smem;
 };
 
 static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t delay, DenseGeom* g) {
     const int64_t B = h->B;
+    const int64_t Bpad = (B + 7) / 8 * 8;
     int64_t R = sp->panel_rows;
     if (R <= 0) R = 4096 / B;                       // ~32 KB panels
     R = (R + 31) / 32 * 32;
     R = std::max<int64_t>(32, std::min<int64_t>(R, 256));
+    while (R > 32 && (R / 32) * 2 * Bpad > 512) R -= 32;  // one panel must fit a TMEM lane quarter
     const int64_t mr = (h->m + 31) / 32 * 32;
     if (R > mr) R = mr;
     const int64_t G = (h->m + R - 1) / R;
+    const int64_t cols_per_slot = (R / 32) * 2 * Bpad;
+    const int TS = (int)std::min<int64_t>(kMaxTmemSlots, 512 / cols_per_slot);
     const size_t panel = sizeof(double) * R * B;
-    const size_t fixed = sizeof(double) * (kDotWarps * R + kAxpyWarps * B) + 1024;
+    const size_t fixed = sizeof(double) * kPairs * (Bpad + R) + sizeof(StageMeta) * kPairs * TS +
+                         sizeof(uint64_t) * 2 * kPairs * TS + 64;
     int NS = sp->stages;
-    if (NS <= 0) NS = (int)std::min<int64_t>(16, std::max<int64_t>(2, (int64_t)((220 * 1024 - fixed) / panel)));
+    if (NS <= 0) {
+        NS = (int)((200 * 1024 - fixed) / (panel + sizeof(StageMeta) + 2 * sizeof(uint64_t)));
+        NS = std::min(16, NS);
+    }
+    NS = NS / kPairs * kPairs;
+    if (NS < kPairs) return h->fail(ASY_ERR_INVALID, "panel too large: need at least %d stages", kPairs);
     const size_t smem = panel * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t));
     if (smem > 227 * 1024)
         return h->fail(ASY_ERR_INVALID, "panel_rows*block_size*stages too large for shared memory (%zu B)", smem);
@@ -560,12 +570,12 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_async_kernel, kDenseThreads, smem));
     if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense async kernel does not fit on an SM");
-    int grid = occ * h->sms;
+    int grid = h->sms;  // one CTA per SM: it owns the SM's whole TMEM (512 columns)
     // enough workers to keep ~2x the delay window of panels in flight, never more
     const int64_t want = (2 * (delay + 1) * G + NS - 1) / NS;
     if (want < grid) grid = (int)std::max<int64_t>(1, want);
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
-    g->R = R; g->G = G; g->NS = NS; g->grid = grid; g->smem = smem;
+    g->R = R; g->G = G; g->NS = NS; g->TS = TS; g->Bpad = (int)Bpad; g->grid = grid; g->smem = smem;
     return ASY_OK;
 }
 
@@ -605,7 +615,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc); P.dxr = P_<double>(h->dxr);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
     P.ready = P_<long long>(h->ready); P.done = P_<long long>(h->done); P.ver = P_<unsigned>(h->ver);
-    P.slots = slots; P.Bmax = Bmax; P.stages = geo.NS;
+    P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad; P.stages = geo.NS; P.tslots = geo.TS;
 
     dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk * G), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();

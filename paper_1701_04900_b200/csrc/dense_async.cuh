@@ -6,20 +6,26 @@
 // where sequence k updates block b = schedule(k) (S.1) and panel p covers
 // rows [p*R, p*R+R) of that block's columns A_b: an R x B tile loaded by one
 // 2-D TMA (cp.async.bulk.tensor, OOB rows/columns zero-filled) into a stage of
-// an NS-deep shared-memory ring.  A panel is read from HBM exactly once and
-// used for both the dot and the axpy.
+// an NS-deep shared-memory ring.  A panel is read from HBM exactly once.
 //
-// Warp roles (every role is per-warp, so 4 panels can be in each phase):
-//   warp 0 (lane 0)  producer: claim t, arm the stage mbarrier, issue the TMA;
-//   warps 1-4        dot: stage `it` is taken by dot warp it%4.  Guards, then
-//                    w = phi'(r) on the panel rows (inconsistent read of the
-//                    shared residual), A_{b,p}^T w (lane = rows, 32 column
-//                    accumulators, butterfly transpose-reduction), publish;
-//                    the LAST of the G panels of sequence k solves the block
-//                    subproblem (Eq. 2, closed form) and applies (S.4) to x_b;
-//   warps 5-8        axpy: stage `it` is taken by axpy warp it%4.  Wait for
-//                    dx_b, push A_{b,p} dx_b into r (red.add), free the stage,
-//                    then publish completion.
+// Warp roles.  Four "pairs" d = 0..3; pair d owns smem stages st = d (mod 4)
+// and the TMEM lane quarter [32d, 32d+32):
+//   warp 8 (lane 0)   producer: claim t, arm the stage mbarrier, issue the TMA;
+//   warp 4+d  (dot)   guards, w = phi'(r) on the panel rows (inconsistent read
+//                     of the shared residual), then one pass over the panel:
+//                     every row goes smem -> registers -> (FMA into 32 column
+//                     accumulators) and registers -> TMEM (tcgen05.st), after
+//                     which the smem stage is released at once; butterfly
+//                     transpose-reduction, publish the partial A_{b,p}^T w; the
+//                     LAST of the G panels of sequence k solves the block
+//                     subproblem (Eq. 2, closed form) and applies (S.4) to x_b;
+//   warp d    (axpy)  waits for dx_b, reads the panel back from TMEM
+//                     (tcgen05.ld), pushes A_{b,p} dx_b into r (red.add),
+//                     frees the TMEM slot and publishes completion.
+// TMEM (256 KB/SM) thus holds the panels that wait for their block's dx, so
+// the 227 KB of shared memory only covers load latency: the in-flight
+// capacity per SM is smem + TMEM, which is what HBM-rate streaming with a
+// cross-CTA reduction in the middle of every block update needs.
 // Guards (all point to strictly older sequences -> deadlock free with
 // co-resident CTAs):
 //   * D4 freshness [PAPER.md:233]: the panel of block b is not read before the
@@ -36,10 +42,11 @@
 
 namespace asy {
 
-constexpr int kDotWarps = 4;
-constexpr int kAxpyWarps = 4;
-constexpr int kDenseThreads = 32 * (1 + kDotWarps + kAxpyWarps);
+constexpr int kPairs = 4;
+constexpr int kDenseThreads = 32 * (2 * kPairs + 1);
+constexpr int kProducerWarp = 2 * kPairs;
 constexpr int kMaxRowsPerLane = 8;  // R <= 256 (one TMA box per panel)
+constexpr int kMaxTmemSlots = 8;
 
 struct DenseAsyncParams {
     int64_t m, n;
@@ -70,8 +77,10 @@ struct DenseAsyncParams {
     long long* done;     // [S]
     unsigned* ver;       // [nblk*G]
     int64_t slots;       // power of two
-    int32_t Bmax;
-    int32_t stages;
+    int32_t Bmax;        // = B
+    int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
+    int32_t stages;      // multiple of kPairs
+    int32_t tslots;      // TMEM slots per pair
 };
 
 struct StageMeta {
@@ -118,6 +127,65 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     return v;
 }
 
+// ---- TMEM (tcgen05) ---------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc_512(uint32_t* dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst_smem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_512(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 8 doubles (16 x b32 columns) of this thread's TMEM lane
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const double* v) {
+    uint32_t u[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
+        u[2 * i] = (uint32_t)b;
+        u[2 * i + 1] = (uint32_t)(b >> 32);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]), "r"(u[8]),
+        "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+          "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ double u2d(uint32_t lo, uint32_t hi) {
+    return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+
+// Butterfly reduce-scatter over 16 columns: in: v[c] = this lane's partial of
+// column c; out: lanes l and l^16 return the warp total of column l & 15.
+__device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o];
+            const double keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
 // Butterfly reduce-scatter: in: v[c] = this lane's partial of column c (32 columns);
 // out: the returned value on lane l is the warp total of column l.  31 shuffles.
 __device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
@@ -138,64 +206,89 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int NS = P.stages;
+    const int TS = P.tslots;
     const int R = (int)P.R;
-    const int Bmax = P.Bmax;
+    const int Bmax = P.Bmax, Bpad = P.Bpad;
     const size_t PANEL = (size_t)R * Bmax;  // doubles per stage
-    double* panels = reinterpret_cast<double*>(smem_raw);             // NS * PANEL
-    double* wbuf = panels + NS * PANEL;                               // kDotWarps * R
-    double* dxs = wbuf + kDotWarps * R;                               // kAxpyWarps * Bmax
-    StageMeta* meta = reinterpret_cast<StageMeta*>(dxs + kAxpyWarps * Bmax);
-    uint64_t* full = reinterpret_cast<uint64_t*>(meta + NS);
-    uint64_t* empty = full + NS;
+    double* panels = reinterpret_cast<double*>(smem_raw);                       // NS * PANEL
+    double* dxs = panels + NS * PANEL;                                          // kPairs * Bpad
+    double* wbuf = dxs + kPairs * Bpad;                                         // kPairs * R
+    StageMeta* meta = reinterpret_cast<StageMeta*>(wbuf + kPairs * R);         // NS
+    StageMeta* tmeta = meta + NS;                                               // kPairs * TS
+    uint64_t* full = reinterpret_cast<uint64_t*>(tmeta + kPairs * TS);          // NS
+    uint64_t* empty = full + NS;                                                // NS
+    uint64_t* tfull = empty + NS;                                               // kPairs * TS
+    uint64_t* tempty = tfull + kPairs * TS;                                     // kPairs * TS
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + kPairs * TS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        mbar_fence_init();
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
-    }
-    __syncthreads();
-    const int rows_per_lane = R / 32;
-
-    if (warp == 0) {
-        // ------------------------------------------------------------------ producer
-        if (lane != 0) return;
-        const uint64_t pol = policy_evict_first();
-        const uint32_t box_bytes = (uint32_t)(PANEL * 8);
-        int ends = 0;
-        for (long long it = 0;; ++it) {
-            const int st = (int)(it % NS);
-            if (it >= NS) mbar_wait(&empty[st], (uint32_t)(((it / NS) - 1) & 1));
-            StageMeta& md = meta[st];
-            long long t = -1;
-            if (ends == 0) {
-                t = (long long)atomicAdd(P.counter, 1ull);
-                if (t >= P.T) t = -1;
-            }
-            if (t < 0) {  // one end marker for each of the 4 dot / 4 axpy warps
-                md.t = -1;
-                mbar_arrive(&full[st]);
-                if (++ends == 4) break;
-                continue;
-            }
-            const long long k = t / P.G, p = t - k * P.G;
-            const long long b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + k);
-            md.t = t; md.k = k; md.b = b; md.p = p;
-            mbar_arrive_expect_tx(&full[st], box_bytes);
-            tma_load_2d(panels + st * PANEL, &tmap, (int)(p * R), (int)(b * P.B), &full[st], pol);
+    if (warp == kProducerWarp) {
+        tmem_alloc_512(tmem_base_s);
+        if (lane == 0) {
+            for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+            for (int s = 0; s < kPairs * TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 1); }
+            mbar_fence_init();
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
         }
-        return;
     }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_s;
+    const int rows_per_lane = R / 32;
+    const int cols_per_row = 2 * Bpad;                      // b32 TMEM columns per panel row
+    const int cols_per_slot = rows_per_lane * cols_per_row;
 
-    if (warp <= kDotWarps) {
+    if (warp == kProducerWarp) {
+        // ------------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            const uint32_t box_bytes = (uint32_t)(PANEL * 8);
+            int ends = 0;
+            for (long long it = 0;; ++it) {
+                const int st = (int)(it % NS);
+                if (it >= NS) mbar_wait(&empty[st], (uint32_t)(((it / NS) - 1) & 1));
+                StageMeta& md = meta[st];
+                long long t = -1;
+                if (ends == 0) {
+                    t = (long long)atomicAdd(P.counter, 1ull);
+                    if (t >= P.T) t = -1;
+                }
+                if (t < 0) {  // one end marker for each pair (consecutive iterations)
+                    md.t = -1;
+                    mbar_arrive(&full[st]);
+                    if (++ends == kPairs) break;
+                    continue;
+                }
+                const long long k = t / P.G, p = t - k * P.G;
+                const long long b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + k);
+                md.t = t; md.k = k; md.b = b; md.p = p;
+                mbar_arrive_expect_tx(&full[st], box_bytes);
+                tma_load_2d(panels + st * PANEL, &tmap, (int)(p * R), (int)(b * P.B), &full[st], pol);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kPairs) {
         // ------------------------------------------------------------------ dot warps
-        const int dw = warp - 1;
-        double* wv = wbuf + dw * R;
-        for (long long it = dw;; it += kDotWarps) {
+        const int d = warp - kPairs;
+        const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
+        double* wsm = wbuf + d * R;
+        for (long long j = 0;; ++j) {
+            const long long it = j * kPairs + d;
             const int st = (int)(it % NS);
+            const int ts = (int)(j % TS);
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
             const StageMeta md = meta[st];
-            if (md.t < 0) break;
+            // TMEM slot free?
+            if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
+            tc_fence_after();
+            if (md.t < 0) {
+                if (lane == 0) {
+                    tmeta[d * TS + ts].t = -1;
+                    mbar_arrive(&tfull[d * TS + ts]);
+                }
+                break;
+            }
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
             const long long c0 = b * P.B;
@@ -215,43 +308,51 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 fence_acqrel_gpu();
             }
             __syncwarp();
-            // w = phi'(r) on the panel rows: issue all loads first, then compute
+            // w = phi'(r) on this lane's rows: issue all loads first, then compute
             const long long r0 = p * R;
-            double rv[kMaxRowsPerLane];
+            {
+                double rv[kMaxRowsPerLane];
 #pragma unroll
-            for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                const long long row = r0 + lane + 32 * q;
-                rv[q] = (q < rows_per_lane && row < P.m) ? ld_relaxed_f64(&P.r[row]) : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                if (q < rows_per_lane) {
+                for (int q = 0; q < kMaxRowsPerLane; ++q) {
                     const long long row = r0 + lane + 32 * q;
-                    wv[lane + 32 * q] = row < P.m ? loss_prime(P.S, rv[q], P.aux[row]) : 0.0;
+                    rv[q] = (q < rows_per_lane && row < P.m) ? ld_relaxed_f64(&P.r[row]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                    const long long row = r0 + lane + 32 * q;
+                    if (q < rows_per_lane) wsm[lane + 32 * q] = row < P.m ? loss_prime(P.S, rv[q], P.aux[row]) : 0.0;
                 }
             }
-            __syncwarp();
-            // A_{b,p}^T w, 32 columns at a time
-            for (int g0 = 0; g0 < nc; g0 += 32) {
-                const int ncg = (nc - g0) < 32 ? (nc - g0) : 32;
-                double acc[32];
+            // one pass over the panel: smem -> regs -> {FMA, TMEM}
+            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
+            for (int g0 = 0; g0 < Bpad; g0 += 16) {
+                const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;  // valid smem columns in group
+                const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;  // TMEM columns (doubles) in group
+                double acc[16];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+                for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+#pragma unroll 1
                 for (int q = 0; q < rows_per_lane; ++q) {
                     const int i = lane + 32 * q;
-                    const double w = wv[i];
+                    const double w = wsm[i];
                     const double* a = pan + (size_t)g0 * R + i;
+                    double v[16];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (c < ncg) acc[c] = fma(a[(size_t)c * R], w, acc[c]);
+                    for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) acc[c] = fma(v[c], w, acc[c]);
+                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * g0);
+                    tmem_st8(trow, v);
+                    if (npg > 8) tmem_st8(trow + 16, v + 8);
                 }
-                const double colsum = transpose_reduce32(acc, lane);
-                if (lane < ncg) {
+                const double colsum = transpose_reduce16(acc, lane);
+                if (lane < ncg && g0 + lane < nc) {
                     if (P.deterministic) P.part[p * Bmax + g0 + lane] = colsum;
                     else atomicAdd(&P.gacc[slot * Bmax + g0 + lane], colsum);
                 }
             }
             __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);  // panel now lives in TMEM: free the smem stage
             unsigned last = 0;
             if (lane == 0) last = atom_add_acqrel_u32(&P.arrive[slot], 1u) == (unsigned)(P.G - 1);
             last = __shfl_sync(0xffffffffu, last, 0);
@@ -272,71 +373,86 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         g = ld_relaxed_f64(&P.gacc[slot * Bmax + c]);
                         P.gacc[slot * Bmax + c] = 0.0;
                     }
-                    const long long j = c0 + c;
-                    const double y = ld_relaxed_f64(&P.x[j]);
-                    const double xh = best_response(P.S, g, y, P.tau[j], j);
+                    const long long jj = c0 + c;
+                    const double y = ld_relaxed_f64(&P.x[jj]);
+                    const double xh = best_response(P.S, g, y, P.tau[jj], jj);
                     const double xn = y + P.gamma * (xh - y);
-                    P.x[j] = xn;
+                    P.x[jj] = xn;
                     P.dxr[slot * Bmax + c] = xn - y;
                 }
                 __syncwarp();
                 if (lane == 0) st_release_s64(&P.ready[slot], k);
             }
-        }
-        return;
-    }
-
-    // ---------------------------------------------------------------------- axpy warps
-    const int aw = warp - 1 - kDotWarps;
-    double* dv = dxs + aw * Bmax;
-    for (long long it = aw;; it += kAxpyWarps) {
-        const int st = (int)(it % NS);
-        mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
-        const StageMeta md = meta[st];
-        if (md.t < 0) break;
-        const long long k = md.k, b = md.b, p = md.p;
-        const long long slot = k & (P.slots - 1);
-        const long long c0 = b * P.B;
-        const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
-        const double* pan = panels + st * PANEL;
-        if (lane == 0) spin_until_ge(&P.ready[slot], k);
-        __syncwarp();
-        bool nz = false;
-        for (int c = lane; c < Bmax; c += 32) {
-            const double d = c < nc ? ld_relaxed_f64(&P.dxr[slot * Bmax + c]) : 0.0;
-            dv[c] = d;
-            nz |= d != 0.0;
-        }
-        nz = __any_sync(0xffffffffu, nz);
-        __syncwarp();
-        const long long r0 = p * R;
-        if (nz) {
-            // rows_per_lane independent FMA chains (one per row), dx broadcast from smem
-            double d[kMaxRowsPerLane];
-#pragma unroll
-            for (int q = 0; q < kMaxRowsPerLane; ++q) d[q] = 0.0;
-            for (int c = 0; c < nc; ++c) {
-                const double dc = dv[c];
-                const double* a = pan + (size_t)c * R + lane;
-#pragma unroll
-                for (int q = 0; q < kMaxRowsPerLane; ++q)
-                    if (q < rows_per_lane) d[q] = fma(a[32 * q], dc, d[q]);
-            }
-#pragma unroll
-            for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                const long long row = r0 + lane + 32 * q;
-                if (q < rows_per_lane && row < P.m && d[q] != 0.0) atomicAdd(&P.r[row], d[q]);
+            // hand the TMEM slot to the axpy warp of this pair
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                tmeta[d * TS + ts] = md;
+                mbar_arrive(&tfull[d * TS + ts]);
             }
         }
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&empty[st]);  // smem stage free; the red.adds may still be in flight
-            fence_acqrel_gpu();       // ... and are performed before the completion counters move
-            atomicAdd(&P.ver[b * P.G + p], 1u);
-            const unsigned old = atomicAdd(&P.consumed[slot], 1u);
-            if (old == (unsigned)(P.G - 1)) st_release_s64(&P.done[slot], k);
+    } else {
+        // ------------------------------------------------------------------ axpy warps
+        const int d = warp;
+        const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
+        double* dv = dxs + d * Bpad;
+        for (long long j = 0;; ++j) {
+            const int ts = (int)(j % TS);
+            mbar_wait(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1));
+            tc_fence_after();
+            const StageMeta md = tmeta[d * TS + ts];
+            if (md.t < 0) break;
+            const long long k = md.k, b = md.b, p = md.p;
+            const long long slot = k & (P.slots - 1);
+            const long long c0 = b * P.B;
+            const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
+            if (lane == 0) spin_until_ge(&P.ready[slot], k);
+            __syncwarp();
+            bool nz = false;
+            for (int c = lane; c < Bpad; c += 32) {
+                const double dd = c < nc ? ld_relaxed_f64(&P.dxr[slot * Bmax + c]) : 0.0;
+                dv[c] = dd;
+                nz |= dd != 0.0;
+            }
+            nz = __any_sync(0xffffffffu, nz);
+            __syncwarp();
+            const long long r0 = p * R;
+            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
+            if (nz) {
+#pragma unroll 1
+                for (int q = 0; q < kMaxRowsPerLane; ++q) {
+                    if (q < rows_per_lane) {
+                        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+                        for (int c8 = 0; c8 < Bpad; c8 += 8) {
+                            uint32_t u[16];
+                            tmem_ld8(tslot + (uint32_t)(q * cols_per_row + 2 * c8), u);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                acc4[i & 3] = fma(u2d(u[2 * i], u[2 * i + 1]), dv[c8 + i], acc4[i & 3]);
+                        }
+                        const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+                        const long long row = r0 + lane + 32 * q;
+                        if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free; the red.adds may still be in flight
+                fence_acqrel_gpu();                 // ... and are performed before the completion counters move
+                atomicAdd(&P.ver[b * P.G + p], 1u);
+                const unsigned old = atomicAdd(&P.consumed[slot], 1u);
+                if (old == (unsigned)(P.G - 1)) st_release_s64(&P.done[slot], k);
+            }
         }
     }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kProducerWarp) tmem_dealloc_512(tmem_base);
 }
 
 }  // namespace asy
