@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -55,7 +56,7 @@ struct asy_handle {
     int64_t gemv_chunks = 1, gemv_cpc = 1;
     Dev red_part, red_out;                // reduction buffers
     // async state
-    Dev counter, gacc, dxr, dpart, arrive, consumed, ready, done, ver;
+    Dev counter, gacc, dpart, arrive, consumed, done, ver;
     int64_t slots = 0;
     int64_t epochs = 0;                   // sweeps since reset (schedule epoch)
 
@@ -137,7 +138,7 @@ static int64_t next_pow2(int64_t v) {
 static void free_problem(asy_handle* h) {
     Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
                   &h->tau, &h->lo, &h->hi, &h->x, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
-                  &h->part, &h->gacc, &h->dxr, &h->dpart, &h->arrive, &h->consumed, &h->ready, &h->done,
+                  &h->part, &h->gacc, &h->dpart, &h->arrive, &h->consumed, &h->done,
                   &h->ver};
     for (Dev* d : all) dev_free(*d);
     h->has_problem = false;
@@ -555,7 +556,7 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int TS = (int)std::min<int64_t>(kMaxTmemSlots, 512 / cols_per_slot);
     const size_t panel = sizeof(double) * R * B;
     const size_t fixed = sizeof(double) * kPairs * (Bpad + R) + sizeof(StageMeta) * kPairs * TS +
-                         sizeof(uint64_t) * 2 * kPairs * TS + 64;
+                         sizeof(uint64_t) * 2 * kPairs * TS + (sizeof(StageMeta) + 2 * sizeof(uint64_t)) * kQueue + 64;
     int NS = sp->stages;
     if (NS <= 0) {
         NS = (int)((200 * 1024 - fixed) / (panel + sizeof(StageMeta) + 2 * sizeof(uint64_t)));
@@ -599,25 +600,32 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
 
     const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
     TRY(dev_alloc(h, h->gacc, sizeof(double) * slots * Bmax));
-    TRY(dev_alloc(h, h->dxr, sizeof(double) * slots * Bmax));
     TRY(dev_alloc(h, h->dpart, sizeof(double) * G * Bmax));
     TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
     TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots));
-    TRY(dev_alloc(h, h->ready, sizeof(long long) * slots));
     TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
-    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk * G));
+    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk));
 
     DenseAsyncParams P{};
     P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x); P.tau = P_<double>(h->tau);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
     P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
-    P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc); P.dxr = P_<double>(h->dxr);
+    P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
-    P.ready = P_<long long>(h->ready); P.done = P_<long long>(h->done); P.ver = P_<unsigned>(h->ver);
+    P.done = P_<long long>(h->done); P.xver = P_<unsigned>(h->ver);
     P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad; P.stages = geo.NS; P.tslots = geo.TS;
 
-    dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk * G), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    // debug trace (env ASY_TRACE=<subtasks>, ASY_TRACE_FILE=<path>): globaltimer stamps per subtask
+    const char* tr = getenv("ASY_TRACE");
+    Dev trace;
+    if (tr && atoll(tr) > 0) {
+        P.trace_n = std::min<int64_t>(atoll(tr), P.T);
+        TRY(dev_alloc(h, trace, sizeof(unsigned long long) * 8 * P.trace_n));
+        CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 8 * P.trace_n, h->stream));
+        P.trace = P_<unsigned long long>(trace);
+    }
+    dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
     void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));
@@ -627,6 +635,17 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    if (P.trace) {
+        std::vector<unsigned long long> hb(8 * P.trace_n);
+        CK(cudaMemcpy(hb.data(), trace.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
+        const char* fn = getenv("ASY_TRACE_FILE");
+        FILE* f = fopen(fn ? fn : "asy_trace.bin", "wb");
+        if (f) {
+            fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+            fclose(f);
+        }
+        dev_free(trace);
+    }
     return ASY_OK;
 }
 

@@ -10,29 +10,38 @@
 //
 // Warp roles.  Four "pairs" d = 0..3; pair d owns smem stages st = d (mod 4)
 // and the TMEM lane quarter [32d, 32d+32):
-//   warp 8 (lane 0)   producer: claim t, arm the stage mbarrier, issue the TMA;
-//   warp 4+d  (dot)   guards, w = phi'(r) on the panel rows (inconsistent read
-//                     of the shared residual), then one pass over the panel:
-//                     every row goes smem -> registers -> (FMA into 32 column
+//   warp 9 (lane 0)   scheduler: claims subtasks in batches of kClaim from the
+//                     counter, checks the guards below (acquire) and queues
+//                     the admitted subtasks in shared memory;
+//   warp 8 (lane 0)   producer: pops the queue, arms the stage mbarrier and
+//                     issues the TMA;
+//   warp 4+d  (dot)   w = phi'(r) on the panel rows (inconsistent read of the
+//                     shared residual), then one pass over the panel: every
+//                     row goes smem -> registers -> (FMA into 16 column
 //                     accumulators) and registers -> TMEM (tcgen05.st), after
 //                     which the smem stage is released at once; butterfly
-//                     transpose-reduction, publish the partial A_{b,p}^T w; the
-//                     LAST of the G panels of sequence k solves the block
-//                     subproblem (Eq. 2, closed form) and applies (S.4) to x_b;
-//   warp d    (axpy)  waits for dx_b, reads the panel back from TMEM
-//                     (tcgen05.ld), pushes A_{b,p} dx_b into r (red.add),
-//                     frees the TMEM slot and publishes completion.
+//                     transpose-reduction, red.add of the partial A_{b,p}^T w
+//                     into the sequence's accumulator and a release-add of its
+//                     arrival counter;
+//   warp d    (axpy)  waits until all G panels of its sequence arrived, solves
+//                     the block subproblem (Eq. 2, closed form) and (S.4) from
+//                     the accumulated gradient (every panel of the block does
+//                     this redundantly, bit-identically), reads its panel back
+//                     from TMEM (tcgen05.ld), pushes A_{b,p} dx_b into r
+//                     (red.add) and frees the TMEM slot; the LAST of the G
+//                     panels writes x_b, recycles the sequence slot and
+//                     publishes the block / sequence as complete.
 // TMEM (256 KB/SM) thus holds the panels that wait for their block's dx, so
 // the 227 KB of shared memory only covers load latency: the in-flight
 // capacity per SM is smem + TMEM, which is what HBM-rate streaming with a
 // cross-CTA reduction in the middle of every block update needs.
-// Guards (all point to strictly older sequences -> deadlock free with
-// co-resident CTAs):
-//   * D4 freshness [PAPER.md:233]: the panel of block b is not read before the
-//     previous update of b has been applied to those rows (ver[] counters);
+// Guards, checked by the producer before a panel is loaded (all point to
+// strictly older sequences -> deadlock free with co-resident CTAs):
+//   * D4 freshness [PAPER.md:233]: block b is not read before its previous
+//     update is complete -- applied to r and written to x (xver[b]);
 //   * bounded delay D1 [PAPER.md:224]: sequence k does not read before
-//     sequence k - delay - 1 is fully applied (done[] ring);
-//   * slot reuse of the per-sequence accumulators.
+//     sequence k - delay - 1 is complete (done[] ring);
+//   * slot reuse: sequence k's accumulator slot was recycled by k - slots.
 // delay == 0 makes the kernel the sequential (d^k = 0) scheme and, with the
 // fixed-order partial reduction (deterministic = 1), bit-reproducible.
 #pragma once
@@ -43,10 +52,13 @@
 namespace asy {
 
 constexpr int kPairs = 4;
-constexpr int kDenseThreads = 32 * (2 * kPairs + 1);
+constexpr int kDenseThreads = 32 * (2 * kPairs + 2);
 constexpr int kProducerWarp = 2 * kPairs;
+constexpr int kSchedWarp = 2 * kPairs + 1;
+constexpr int kQueue = 4;           // scheduler -> producer queue depth
 constexpr int kMaxRowsPerLane = 8;  // R <= 256 (one TMA box per panel)
 constexpr int kMaxTmemSlots = 8;
+constexpr int kClaim = 4;           // subtasks claimed per atomic
 
 struct DenseAsyncParams {
     int64_t m, n;
@@ -68,20 +80,31 @@ struct DenseAsyncParams {
     int deterministic;
     // synchronisation state (initialised by dense_async_init)
     unsigned long long* counter;
-    double* gacc;        // [S][Bmax]
-    double* dxr;         // [S][Bmax]
-    double* part;        // [G][Bmax] (deterministic mode)
-    unsigned* arrive;    // [S]
-    unsigned* consumed;  // [S]
-    long long* ready;    // [S]
-    long long* done;     // [S]
-    unsigned* ver;       // [nblk*G]
+    double* gacc;        // [S][Bmax]  accumulated A_b^T w of sequence k (slot k mod S)
+    double* part;        // [G][Bmax]  per-panel partials (deterministic mode)
+    unsigned* arrive;    // [S]        panels of the sequence whose partial is published
+    unsigned* consumed;  // [S]        panels of the sequence whose axpy is done
+    long long* done;     // [S]        last complete sequence of the slot
+    unsigned* xver;      // [nblk]     completed updates of block b in this launch
     int64_t slots;       // power of two
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
     int32_t stages;      // multiple of kPairs
     int32_t tslots;      // TMEM slots per pair
+    unsigned long long* trace;  // optional [trace_n][8] globaltimer stamps (debug; null = off)
+    int64_t trace_n;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define ASY_TRACE(P_, t_, slot_)                                                   \
+    do {                                                                           \
+        if ((P_).trace && (t_) >= 0 && (t_) < (P_).trace_n && lane == 0)           \
+            (P_).trace[(t_) * 8 + (slot_)] = gtimer();                             \
+    } while (0)
 
 struct StageMeta {
     long long t, k, b, p;
@@ -93,12 +116,11 @@ __global__ void dense_async_init(DenseAsyncParams P) {
     if (tid == 0) *P.counter = 0ull;
     for (int64_t s = tid; s < P.slots; s += nth) {
         P.arrive[s] = 0u;
-        P.consumed[s] = (unsigned)P.G;
-        P.ready[s] = (long long)s - (long long)P.slots;
+        P.consumed[s] = 0u;
         P.done[s] = (long long)s - (long long)P.slots;
     }
     for (int64_t i = tid; i < P.slots * P.Bmax; i += nth) P.gacc[i] = 0.0;
-    for (int64_t i = tid; i < P.nblk * P.G; i += nth) P.ver[i] = 0u;
+    for (int64_t i = tid; i < P.nblk; i += nth) P.xver[i] = 0u;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
@@ -116,6 +138,9 @@ __device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned* p, unsigned v)
     return old;
 }
 __device__ __forceinline__ void fence_acqrel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_add_release_u32(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ long long ld_relaxed_s64(const long long* p) {
     long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -219,7 +244,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     uint64_t* empty = full + NS;                                                // NS
     uint64_t* tfull = empty + NS;                                               // kPairs * TS
     uint64_t* tempty = tfull + kPairs * TS;                                     // kPairs * TS
-    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + kPairs * TS);
+    uint64_t* qfull = tempty + kPairs * TS;                                     // kQueue
+    uint64_t* qempty = qfull + kQueue;                                          // kQueue
+    StageMeta* queue = reinterpret_cast<StageMeta*>(qempty + kQueue);           // kQueue
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(queue + kQueue);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kProducerWarp) {
@@ -227,6 +255,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         if (lane == 0) {
             for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
             for (int s = 0; s < kPairs * TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 1); }
+            for (int s = 0; s < kQueue; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qempty[s], 1); }
             mbar_fence_init();
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
         }
@@ -245,27 +274,88 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const uint64_t pol = policy_evict_first();
             const uint32_t box_bytes = (uint32_t)(PANEL * 8);
             int ends = 0;
+            long long qi = 0;
             for (long long it = 0;; ++it) {
                 const int st = (int)(it % NS);
                 if (it >= NS) mbar_wait(&empty[st], (uint32_t)(((it / NS) - 1) & 1));
                 StageMeta& md = meta[st];
-                long long t = -1;
+                StageMeta e;
+                e.t = -1;
                 if (ends == 0) {
-                    t = (long long)atomicAdd(P.counter, 1ull);
-                    if (t >= P.T) t = -1;
+                    const int qs = (int)(qi % kQueue);
+                    mbar_wait(&qfull[qs], (uint32_t)((qi / kQueue) & 1));
+                    e = queue[qs];
+                    mbar_arrive(&qempty[qs]);
+                    ++qi;
                 }
-                if (t < 0) {  // one end marker for each pair (consecutive iterations)
+                if (e.t < 0) {  // one end marker for each pair (consecutive iterations)
                     md.t = -1;
                     mbar_arrive(&full[st]);
                     if (++ends == kPairs) break;
                     continue;
                 }
-                const long long k = t / P.G, p = t - k * P.G;
-                const long long b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + k);
-                md.t = t; md.k = k; md.b = b; md.p = p;
+                md = e;
+                ASY_TRACE(P, e.t, 1);
                 mbar_arrive_expect_tx(&full[st], box_bytes);
-                tma_load_2d(panels + st * PANEL, &tmap, (int)(p * R), (int)(b * P.B), &full[st], pol);
+                tma_load_2d(panels + st * PANEL, &tmap, (int)(e.p * R), (int)(e.b * P.B), &full[st], pol);
             }
+        }
+        __syncwarp();
+    } else if (warp == kSchedWarp) {
+        // ------------------------------------------------------------------ scheduler
+        if (lane == 0) {
+            long long qi = 0;
+            auto push = [&](const StageMeta& e) {
+                const int qs = (int)(qi % kQueue);
+                if (qi >= kQueue) mbar_wait(&qempty[qs], (uint32_t)(((qi / kQueue) - 1) & 1));
+                queue[qs] = e;
+                mbar_arrive(&qfull[qs]);
+                ++qi;
+            };
+            for (;;) {
+                const long long tb = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
+                if (tb >= P.T) break;
+                StageMeta e[kClaim];
+                unsigned xv[kClaim];
+                long long ds[kClaim], dw[kClaim];
+#pragma unroll
+                for (int i = 0; i < kClaim; ++i) {
+                    const long long t = tb + i;
+                    e[i].t = t < P.T ? t : -1;
+                    e[i].k = t / P.G;
+                    e[i].p = t - e[i].k * P.G;
+                    e[i].b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + e[i].k);
+                    ASY_TRACE(P, t, 0);
+                }
+                // guards: all loads in flight at once, spin only if needed, one acquire fence
+#pragma unroll
+                for (int i = 0; i < kClaim; ++i) {
+                    const long long k = e[i].k, kd = k - P.delay - 1;
+                    xv[i] = ld_relaxed_u32(&P.xver[e[i].b]);
+                    ds[i] = ld_relaxed_s64(&P.done[k & (P.slots - 1)]);
+                    dw[i] = kd >= 0 ? ld_relaxed_s64(&P.done[kd & (P.slots - 1)]) : kd;
+                }
+                // admit in claim order: a subtask never waits while an older one of this batch is held back
+                bool fenced = false;
+#pragma unroll
+                for (int i = 0; i < kClaim; ++i) {
+                    if (e[i].t < 0) continue;
+                    const long long k = e[i].k, kd = k - P.delay - 1;
+                    const unsigned u = (unsigned)(k / P.nblk);
+                    if (xv[i] < u || ds[i] < k - P.slots || dw[i] < kd) {
+                        spin_until_ge_u32(&P.xver[e[i].b], u);
+                        spin_until_ge(&P.done[k & (P.slots - 1)], k - P.slots);
+                        if (kd >= 0) spin_until_ge(&P.done[kd & (P.slots - 1)], kd);
+                    } else if (!fenced) {
+                        fence_acqrel_gpu();
+                        fenced = true;
+                    }
+                    push(e[i]);
+                }
+            }
+            StageMeta end;
+            end.t = -1; end.k = end.b = end.p = 0;
+            push(end);
         }
         __syncwarp();
     } else if (warp >= kPairs) {
@@ -279,10 +369,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int ts = (int)(j % TS);
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
             const StageMeta md = meta[st];
-            // TMEM slot free?
-            if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
-            tc_fence_after();
             if (md.t < 0) {
+                if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
                 if (lane == 0) {
                     tmeta[d * TS + ts].t = -1;
                     mbar_arrive(&tfull[d * TS + ts]);
@@ -294,20 +382,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const double* pan = panels + st * PANEL;
-            // guards: three independent relaxed loads, one acquire fence
-            if (lane == 0) {
-                const unsigned u = (unsigned)(k / P.nblk);
-                const long long kd = k - P.delay - 1;
-                long long* donep = &P.done[kd & (P.slots - 1)];
-                const long long rdy = ld_relaxed_s64(&P.ready[slot]);
-                const unsigned ver = ld_relaxed_u32(&P.ver[b * P.G + p]);
-                const long long dn = kd >= 0 ? ld_relaxed_s64(donep) : kd;
-                if (rdy < k - P.slots) spin_until_ge(&P.ready[slot], k - P.slots);
-                if (ver < u) spin_until_ge_u32(&P.ver[b * P.G + p], u);
-                if (dn < kd) spin_until_ge(donep, kd);
-                fence_acqrel_gpu();
-            }
-            __syncwarp();
+            ASY_TRACE(P, md.t, 2);
             // w = phi'(r) on this lane's rows: issue all loads first, then compute
             const long long r0 = p * R;
             {
@@ -323,27 +398,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     if (q < rows_per_lane) wsm[lane + 32 * q] = row < P.m ? loss_prime(P.S, rv[q], P.aux[row]) : 0.0;
                 }
             }
-            // one pass over the panel: smem -> regs -> {FMA, TMEM}
-            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
-            for (int g0 = 0; g0 < Bpad; g0 += 16) {
+            // pass 1: A_{b,p}^T w from shared memory and publish -- never waits on TMEM,
+            // so a block's completion is not held back by the TMEM ring
+            for (int g0 = 0; g0 < Bmax; g0 += 16) {
                 const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;  // valid smem columns in group
-                const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;  // TMEM columns (doubles) in group
                 double acc[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) acc[c] = 0.0;
-#pragma unroll 1
+#pragma unroll 2
                 for (int q = 0; q < rows_per_lane; ++q) {
                     const int i = lane + 32 * q;
                     const double w = wsm[i];
                     const double* a = pan + (size_t)g0 * R + i;
-                    double v[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) acc[c] = fma(v[c], w, acc[c]);
-                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * g0);
-                    tmem_st8(trow, v);
-                    if (npg > 8) tmem_st8(trow + 16, v + 8);
+                    for (int c = 0; c < 16; ++c)
+                        if (c < ncg) acc[c] = fma(a[(size_t)c * R], w, acc[c]);
                 }
                 const double colsum = transpose_reduce16(acc, lane);
                 if (lane < ncg && g0 + lane < nc) {
@@ -352,37 +421,29 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);  // panel now lives in TMEM: free the smem stage
-            unsigned last = 0;
-            if (lane == 0) last = atom_add_acqrel_u32(&P.arrive[slot], 1u) == (unsigned)(P.G - 1);
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                // last panel of sequence k: solve the block subproblem (Eq. 2) and apply (S.4)
-                if (lane == 0) {
-                    P.arrive[slot] = 0u;
-                    spin_until_ge_u32(&P.consumed[slot], (unsigned)P.G);  // seq k-S fully applied
-                    P.consumed[slot] = 0u;
+            if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);  // partials before the count
+            ASY_TRACE(P, md.t, 3);
+            // pass 2: park the panel in TMEM (smem -> regs -> tcgen05.st) and free the stage
+            if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
+            tc_fence_after();
+            ASY_TRACE(P, md.t, 4);
+            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
+            for (int g0 = 0; g0 < Bpad; g0 += 16) {
+                const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;
+                const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;
+#pragma unroll 1
+                for (int q = 0; q < rows_per_lane; ++q) {
+                    const double* a = pan + (size_t)g0 * R + lane + 32 * q;
+                    double v[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
+                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * g0);
+                    tmem_st8(trow, v);
+                    if (npg > 8) tmem_st8(trow + 16, v + 8);
                 }
-                __syncwarp();
-                for (int c = lane; c < nc; c += 32) {
-                    double g;
-                    if (P.deterministic) {
-                        g = 0.0;
-                        for (long long q = 0; q < P.G; ++q) g += ld_relaxed_f64(&P.part[q * Bmax + c]);
-                    } else {
-                        g = ld_relaxed_f64(&P.gacc[slot * Bmax + c]);
-                        P.gacc[slot * Bmax + c] = 0.0;
-                    }
-                    const long long jj = c0 + c;
-                    const double y = ld_relaxed_f64(&P.x[jj]);
-                    const double xh = best_response(P.S, g, y, P.tau[jj], jj);
-                    const double xn = y + P.gamma * (xh - y);
-                    P.x[jj] = xn;
-                    P.dxr[slot * Bmax + c] = xn - y;
-                }
-                __syncwarp();
-                if (lane == 0) st_release_s64(&P.ready[slot], k);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);  // panel now lives in TMEM: free the smem stage
             // hand the TMEM slot to the axpy warp of this pair
             tmem_wait_st();
             tc_fence_before();
@@ -407,12 +468,34 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long slot = k & (P.slots - 1);
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
-            if (lane == 0) spin_until_ge(&P.ready[slot], k);
+            ASY_TRACE(P, md.t, 5);
+            // all G partials of sequence k published?
+            if (lane == 0) spin_until_ge_u32(&P.arrive[slot], (unsigned)P.G);
+            ASY_TRACE(P, md.t, 6);
             __syncwarp();
+            // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block
+            double xn[(128 + 31) / 32];
             bool nz = false;
-            for (int c = lane; c < Bpad; c += 32) {
-                const double dd = c < nc ? ld_relaxed_f64(&P.dxr[slot * Bmax + c]) : 0.0;
-                dv[c] = dd;
+#pragma unroll
+            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+                const int c = lane + 32 * s4;
+                double dd = 0.0;
+                xn[s4] = 0.0;
+                if (c < nc) {
+                    double g;
+                    if (P.deterministic) {
+                        g = 0.0;
+                        for (long long q = 0; q < P.G; ++q) g += ld_relaxed_f64(&P.part[q * Bmax + c]);
+                    } else {
+                        g = ld_relaxed_f64(&P.gacc[slot * Bmax + c]);
+                    }
+                    const long long jj = c0 + c;
+                    const double y = ld_relaxed_f64(&P.x[jj]);
+                    const double xh = best_response(P.S, g, y, P.tau[jj], jj);
+                    xn[s4] = y + P.gamma * (xh - y);
+                    dd = xn[s4] - y;
+                }
+                if (c < Bpad) dv[c] = dd;
                 nz |= dd != 0.0;
             }
             nz = __any_sync(0xffffffffu, nz);
@@ -440,12 +523,32 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
+            ASY_TRACE(P, md.t, 7);
+            unsigned last = 0;
             if (lane == 0) {
-                mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free; the red.adds may still be in flight
-                fence_acqrel_gpu();                 // ... and are performed before the completion counters move
-                atomicAdd(&P.ver[b * P.G + p], 1u);
-                const unsigned old = atomicAdd(&P.consumed[slot], 1u);
-                if (old == (unsigned)(P.G - 1)) st_release_s64(&P.done[slot], k);
+                mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free
+                // reads of gacc/x and the red.adds above are performed before the count moves
+                last = atom_add_acqrel_u32(&P.consumed[slot], 1u) == (unsigned)(P.G - 1);
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                // last panel of sequence k: write x_b, recycle the slot, publish completion
+#pragma unroll
+                for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+                    const int c = lane + 32 * s4;
+                    if (c < nc) {
+                        P.x[c0 + c] = xn[s4];
+                        if (!P.deterministic) P.gacc[slot * Bmax + c] = 0.0;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    P.arrive[slot] = 0u;
+                    P.consumed[slot] = 0u;
+                    __threadfence();
+                    st_release_u32(&P.xver[b], (unsigned)(k / P.nblk) + 1u);
+                    st_release_s64(&P.done[slot], k);
+                }
             }
         }
     }
