@@ -51,7 +51,7 @@ struct asy_handle {
     Dev rowptr, csr_col, csr_val;         // CSR transpose (owned)
     Dev b, tau, lo, hi;                   // owned copies
     // state
-    Dev x, r, dx, w, mf, mer, rs, xs;     // rs/xs: scratch residual / iterate for stationarity
+    Dev x, xalt, r, dx, w, mf, mer, rs, xs;  // xalt: 2nd half of the async x double buffer; rs/xs: scratch
     Dev part;                             // GEMV-N partial sums
     int64_t gemv_chunks = 1, gemv_cpc = 1;
     Dev red_part, red_out;                // reduction buffers
@@ -137,7 +137,7 @@ static int64_t next_pow2(int64_t v) {
 // problem-owned buffers (the handle-lifetime ones -- red_part, red_out, counter -- survive)
 static void free_problem(asy_handle* h) {
     Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
-                  &h->tau, &h->lo, &h->hi, &h->x, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
+                  &h->tau, &h->lo, &h->hi, &h->x, &h->xalt, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
                   &h->part, &h->gacc, &h->dpart, &h->arrive, &h->consumed, &h->done,
                   &h->ver};
     for (Dev* d : all) dev_free(*d);
@@ -495,11 +495,12 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
 
     // ---- state
     TRY(dev_alloc(h, h->x, sizeof(double) * h->n));
+    TRY(dev_alloc(h, h->xalt, sizeof(double) * h->n));
     TRY(dev_alloc(h, h->xs, sizeof(double) * h->n));
     TRY(dev_alloc(h, h->dx, sizeof(double) * h->n));
     TRY(dev_alloc(h, h->mf, sizeof(double) * h->n));
     TRY(dev_alloc(h, h->mer, sizeof(double) * h->n));
-    TRY(dev_alloc(h, h->r, sizeof(double) * h->m));
+    TRY(dev_alloc(h, h->r, sizeof(double) * (h->m + 32)));  // padded: bulk copies of residual rows
     TRY(dev_alloc(h, h->rs, sizeof(double) * h->m));
     TRY(dev_alloc(h, h->w, sizeof(double) * (h->m + 2)));
     h->has_problem = true;
@@ -554,9 +555,10 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int64_t G = (h->m + R - 1) / R;
     const int64_t cols_per_slot = (R / 32) * 2 * Bpad;
     const int TS = (int)std::min<int64_t>(kMaxTmemSlots, 512 / cols_per_slot);
-    const size_t panel = sizeof(double) * R * B;
+    const size_t panel = sizeof(double) * R * (B + 1);  // A tile + residual rows
     const size_t fixed = sizeof(double) * kPairs * (Bpad + R) + sizeof(StageMeta) * kPairs * TS +
-                         sizeof(uint64_t) * 2 * kPairs * TS + (sizeof(StageMeta) + 2 * sizeof(uint64_t)) * kQueue + 64;
+                         sizeof(uint64_t) * 2 * kPairs * TS + (sizeof(StageMeta) + 2 * sizeof(uint64_t)) * kQueue +
+                         64;
     int NS = sp->stages;
     if (NS <= 0) {
         NS = (int)((200 * 1024 - fixed) / (panel + sizeof(StageMeta) + 2 * sizeof(uint64_t)));
@@ -599,21 +601,21 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 
     const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
-    TRY(dev_alloc(h, h->gacc, sizeof(double) * slots * Bmax));
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * Bmax));
     TRY(dev_alloc(h, h->dpart, sizeof(double) * G * Bmax));
     TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
     TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots));
-    TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk));
 
     DenseAsyncParams P{};
     P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
-    P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x); P.tau = P_<double>(h->tau);
+    P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
+    P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
     P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
     P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
-    P.done = P_<long long>(h->done); P.xver = P_<unsigned>(h->ver);
+    P.xver = P_<unsigned>(h->ver);
     P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad; P.stages = geo.NS; P.tslots = geo.TS;
 
     // debug trace (env ASY_TRACE=<subtasks>, ASY_TRACE_FILE=<path>): globaltimer stamps per subtask
@@ -625,7 +627,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
         CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 8 * P.trace_n, h->stream));
         P.trace = P_<unsigned long long>(trace);
     }
-    dense_async_init<<<grid_for(std::max<int64_t>(slots * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    dense_async_init<<<grid_for(std::max<int64_t>(2 * slots * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
     void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));
@@ -635,6 +637,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    if (sweeps & 1) std::swap(h->x, h->xalt);  // the updated iterate lives in the other half
     if (P.trace) {
         std::vector<unsigned long long> hb(8 * P.trace_n);
         CK(cudaMemcpy(hb.data(), trace.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));

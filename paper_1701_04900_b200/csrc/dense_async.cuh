@@ -6,7 +6,9 @@
 // where sequence k updates block b = schedule(k) (S.1) and panel p covers
 // rows [p*R, p*R+R) of that block's columns A_b: an R x B tile loaded by one
 // 2-D TMA (cp.async.bulk.tensor, OOB rows/columns zero-filled) into a stage of
-// an NS-deep shared-memory ring.  A panel is read from HBM exactly once.
+// an NS-deep shared-memory ring, together with the R residual rows it needs
+// (1-D bulk copy, read at issue time: the inconsistent read of the shared
+// residual).  A panel is read from HBM exactly once.
 //
 // Warp roles.  Four "pairs" d = 0..3; pair d owns smem stages st = d (mod 4)
 // and the TMEM lane quarter [32d, 32d+32):
@@ -14,34 +16,37 @@
 //                     counter, checks the guards below (acquire) and queues
 //                     the admitted subtasks in shared memory;
 //   warp 8 (lane 0)   producer: pops the queue, arms the stage mbarrier and
-//                     issues the TMA;
-//   warp 4+d  (dot)   w = phi'(r) on the panel rows (inconsistent read of the
-//                     shared residual), then one pass over the panel: every
-//                     row goes smem -> registers -> (FMA into 16 column
-//                     accumulators) and registers -> TMEM (tcgen05.st), after
-//                     which the smem stage is released at once; butterfly
-//                     transpose-reduction, red.add of the partial A_{b,p}^T w
-//                     into the sequence's accumulator and a release-add of its
-//                     arrival counter;
+//                     issues the two bulk copies;
+//   warp 4+d  (dot)   w = phi'(r) on the panel rows, A_{b,p}^T w straight from
+//                     shared memory (lane = rows, 16 column accumulators,
+//                     butterfly transpose-reduction), red.add into the
+//                     sequence's accumulator; parks the panel in TMEM (smem ->
+//                     registers -> tcgen05.st), frees the smem stage and only
+//                     then release-adds the sequence's arrival counter (the
+//                     partials' red.adds have drained meanwhile);
 //   warp d    (axpy)  waits until all G panels of its sequence arrived, solves
-//                     the block subproblem (Eq. 2, closed form) and (S.4) from
-//                     the accumulated gradient (every panel of the block does
-//                     this redundantly, bit-identically), reads its panel back
-//                     from TMEM (tcgen05.ld), pushes A_{b,p} dx_b into r
-//                     (red.add) and frees the TMEM slot; the LAST of the G
-//                     panels writes x_b, recycles the sequence slot and
-//                     publishes the block / sequence as complete.
-// TMEM (256 KB/SM) thus holds the panels that wait for their block's dx, so
-// the 227 KB of shared memory only covers load latency: the in-flight
-// capacity per SM is smem + TMEM, which is what HBM-rate streaming with a
-// cross-CTA reduction in the middle of every block update needs.
-// Guards, checked by the producer before a panel is loaded (all point to
+//                     the block subproblem (Eq. 2, closed form) and applies
+//                     (S.4) -- every panel of the block does this redundantly
+//                     and bit-identically, writing the new x_b into the other
+//                     half of a double-buffered x -- reads its panel back from
+//                     TMEM (tcgen05.ld), pushes A_{b,p} dx_b into r (red.add)
+//                     and frees the TMEM slot; its completion (release-adds of
+//                     the sequence and block counters) is issued one panel
+//                     later, overlapping the next block's wait.
+// No "last panel" role exists: all counters are monotonic (sequence k owns
+// arrival / completion counts ((k/S)+1)*G in slot k mod S), the accumulator is
+// double-buffered per slot use and zeroed by the next use's consumers, and x
+// is double-buffered per epoch.
+// TMEM (256 KB/SM) holds the panels that wait for their block's dx, so the
+// 227 KB of shared memory only covers load latency: in-flight capacity per SM
+// is smem + TMEM.
+// Guards, checked by the scheduler before a panel is loaded (all point to
 // strictly older sequences -> deadlock free with co-resident CTAs):
 //   * D4 freshness [PAPER.md:233]: block b is not read before its previous
-//     update is complete -- applied to r and written to x (xver[b]);
+//     update is complete -- applied to r and written to x (xver[b] = u*G);
 //   * bounded delay D1 [PAPER.md:224]: sequence k does not read before
-//     sequence k - delay - 1 is complete (done[] ring);
-//   * slot reuse: sequence k's accumulator slot was recycled by k - slots.
+//     sequence k - delay - 1 is complete;
+//   * slot reuse: sequence k - S (previous user of the slot) is complete.
 // delay == 0 makes the kernel the sequential (d^k = 0) scheme and, with the
 // fixed-order partial reduction (deterministic = 1), bit-reproducible.
 #pragma once
@@ -52,9 +57,9 @@
 namespace asy {
 
 constexpr int kPairs = 4;
-constexpr int kDenseThreads = 32 * (2 * kPairs + 2);
 constexpr int kProducerWarp = 2 * kPairs;
 constexpr int kSchedWarp = 2 * kPairs + 1;
+constexpr int kDenseThreads = 32 * (2 * kPairs + 2);
 constexpr int kQueue = 4;           // scheduler -> producer queue depth
 constexpr int kMaxRowsPerLane = 8;  // R <= 256 (one TMA box per panel)
 constexpr int kMaxTmemSlots = 8;
@@ -66,9 +71,10 @@ struct DenseAsyncParams {
     int64_t nblk;   // number of blocks
     int64_t R;      // panel rows (multiple of 32, <= 256) = TMA box rows
     int64_t G;      // panels per block
-    double* r;      // shared residual (LS: Ax-b, logistic: Ax)
+    double* r;      // shared residual (LS: Ax-b, logistic: Ax); >= m+32 entries
     const double* aux;  // b (LS) or y (logistic)
-    double* x;
+    double* x0;     // x buffer read in even local epochs (written in odd ones)
+    double* x1;     // x buffer read in odd local epochs
     const double* tau;
     Scalars S;
     double gamma;
@@ -80,12 +86,11 @@ struct DenseAsyncParams {
     int deterministic;
     // synchronisation state (initialised by dense_async_init)
     unsigned long long* counter;
-    double* gacc;        // [S][Bmax]  accumulated A_b^T w of sequence k (slot k mod S)
+    double* gacc;        // [S][2][Bmax] accumulated A_b^T w; sequence k uses [k mod S][(k/S) & 1]
     double* part;        // [G][Bmax]  per-panel partials (deterministic mode)
-    unsigned* arrive;    // [S]        panels of the sequence whose partial is published
-    unsigned* consumed;  // [S]        panels of the sequence whose axpy is done
-    long long* done;     // [S]        last complete sequence of the slot
-    unsigned* xver;      // [nblk]     completed updates of block b in this launch
+    unsigned* arrive;    // [S]        monotonic: published panels of all users of the slot
+    unsigned* consumed;  // [S]        monotonic: completed panels of all users of the slot
+    unsigned* xver;      // [nblk]     monotonic: completed panels of all updates of block b
     int64_t slots;       // power of two
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
@@ -110,6 +115,7 @@ struct StageMeta {
     long long t, k, b, p;
 };
 
+
 __global__ void dense_async_init(DenseAsyncParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -117,9 +123,8 @@ __global__ void dense_async_init(DenseAsyncParams P) {
     for (int64_t s = tid; s < P.slots; s += nth) {
         P.arrive[s] = 0u;
         P.consumed[s] = 0u;
-        P.done[s] = (long long)s - (long long)P.slots;
     }
-    for (int64_t i = tid; i < P.slots * P.Bmax; i += nth) P.gacc[i] = 0.0;
+    for (int64_t i = tid; i < 2 * P.slots * P.Bmax; i += nth) P.gacc[i] = 0.0;
     for (int64_t i = tid; i < P.nblk; i += nth) P.xver[i] = 0u;
 }
 
@@ -131,16 +136,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
-
-__device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
+__device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
-__device__ __forceinline__ void fence_acqrel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void red_add_release_u32(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void fence_acqrel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ long long ld_relaxed_s64(const long long* p) {
     long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -182,7 +188,7 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const double* v) {
         "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[16]) {
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* u) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
         "%14, %15}, [%16];"
@@ -211,22 +217,6 @@ __device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
-// Butterfly reduce-scatter: in: v[c] = this lane's partial of column c (32 columns);
-// out: the returned value on lane l is the warp total of column l.  31 shuffles.
-__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-            const double send = up ? v[i] : v[i + o];
-            const double keep = up ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-    return v[0];
-}
-
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -234,20 +224,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     const int TS = P.tslots;
     const int R = (int)P.R;
     const int Bmax = P.Bmax, Bpad = P.Bpad;
-    const size_t PANEL = (size_t)R * Bmax;  // doubles per stage
-    double* panels = reinterpret_cast<double*>(smem_raw);                       // NS * PANEL
-    double* dxs = panels + NS * PANEL;                                          // kPairs * Bpad
+    const size_t PANEL = (size_t)R * Bmax;   // doubles of A per stage
+    const size_t STAGE = PANEL + R;          // + the R residual rows
+    double* stages = reinterpret_cast<double*>(smem_raw);                       // NS * STAGE
+    double* dxs = stages + NS * STAGE;                                          // kPairs * Bpad
     double* wbuf = dxs + kPairs * Bpad;                                         // kPairs * R
     StageMeta* meta = reinterpret_cast<StageMeta*>(wbuf + kPairs * R);         // NS
     StageMeta* tmeta = meta + NS;                                               // kPairs * TS
-    uint64_t* full = reinterpret_cast<uint64_t*>(tmeta + kPairs * TS);          // NS
+    StageMeta* queue = tmeta + kPairs * TS;                                     // kQueue
+    uint64_t* full = reinterpret_cast<uint64_t*>(queue + kQueue);               // NS
     uint64_t* empty = full + NS;                                                // NS
     uint64_t* tfull = empty + NS;                                               // kPairs * TS
     uint64_t* tempty = tfull + kPairs * TS;                                     // kPairs * TS
     uint64_t* qfull = tempty + kPairs * TS;                                     // kQueue
     uint64_t* qempty = qfull + kQueue;                                          // kQueue
-    StageMeta* queue = reinterpret_cast<StageMeta*>(qempty + kQueue);           // kQueue
-    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(queue + kQueue);
+    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + kQueue);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kProducerWarp) {
@@ -296,8 +287,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
                 md = e;
                 ASY_TRACE(P, e.t, 1);
-                mbar_arrive_expect_tx(&full[st], box_bytes);
-                tma_load_2d(panels + st * PANEL, &tmap, (int)(e.p * R), (int)(e.b * P.B), &full[st], pol);
+                const long long r0 = e.p * R;
+                const long long nr = (P.m - r0) < R ? (P.m - r0) : R;
+                const uint32_t rbytes = (uint32_t)(((nr + 1) & ~1ll) * 8);
+                double* dst = stages + st * STAGE;
+                mbar_arrive_expect_tx(&full[st], box_bytes + rbytes);
+                tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
+                bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
             }
         }
         __syncwarp();
@@ -327,13 +323,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     e[i].b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + e[i].k);
                     ASY_TRACE(P, t, 0);
                 }
-                // guards: all loads in flight at once, spin only if needed, one acquire fence
+                // guards: all loads in flight at once
+                unsigned cs[kClaim], cw[kClaim];
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long k = e[i].k, kd = k - P.delay - 1;
                     xv[i] = ld_relaxed_u32(&P.xver[e[i].b]);
-                    ds[i] = ld_relaxed_s64(&P.done[k & (P.slots - 1)]);
-                    dw[i] = kd >= 0 ? ld_relaxed_s64(&P.done[kd & (P.slots - 1)]) : kd;
+                    cs[i] = ld_relaxed_u32(&P.consumed[k & (P.slots - 1)]);
+                    cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[kd & (P.slots - 1)]) : 0u;
                 }
                 // admit in claim order: a subtask never waits while an older one of this batch is held back
                 bool fenced = false;
@@ -341,11 +338,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 for (int i = 0; i < kClaim; ++i) {
                     if (e[i].t < 0) continue;
                     const long long k = e[i].k, kd = k - P.delay - 1;
-                    const unsigned u = (unsigned)(k / P.nblk);
-                    if (xv[i] < u || ds[i] < k - P.slots || dw[i] < kd) {
-                        spin_until_ge_u32(&P.xver[e[i].b], u);
-                        spin_until_ge(&P.done[k & (P.slots - 1)], k - P.slots);
-                        if (kd >= 0) spin_until_ge(&P.done[kd & (P.slots - 1)], kd);
+                    const unsigned G = (unsigned)P.G;
+                    const unsigned need_x = (unsigned)(k / P.nblk) * G;             // previous update of b
+                    const unsigned need_s = (unsigned)(k / P.slots) * G;            // seq k - S complete
+                    const unsigned need_w = kd >= 0 ? (unsigned)(kd / P.slots + 1) * G : 0u;  // seq kd complete
+                    if (xv[i] < need_x || cs[i] < need_s || cw[i] < need_w) {
+                        spin_until_ge_u32(&P.xver[e[i].b], need_x);
+                        spin_until_ge_u32(&P.consumed[k & (P.slots - 1)], need_s);
+                        if (kd >= 0) spin_until_ge_u32(&P.consumed[kd & (P.slots - 1)], need_w);
                     } else if (!fenced) {
                         fence_acqrel_gpu();
                         fenced = true;
@@ -379,27 +379,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
+            double* gacc = P.gacc + (slot * 2 + ((k / P.slots) & 1)) * Bmax;
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
-            const double* pan = panels + st * PANEL;
+            const double* pan = stages + st * STAGE;
+            const double* rs = pan + PANEL;
             ASY_TRACE(P, md.t, 2);
-            // w = phi'(r) on this lane's rows: issue all loads first, then compute
+            // w = phi'(r) on the panel rows (residual rows arrived with the panel)
             const long long r0 = p * R;
-            {
-                double rv[kMaxRowsPerLane];
-#pragma unroll
-                for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                    const long long row = r0 + lane + 32 * q;
-                    rv[q] = (q < rows_per_lane && row < P.m) ? ld_relaxed_f64(&P.r[row]) : 0.0;
-                }
-#pragma unroll
-                for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                    const long long row = r0 + lane + 32 * q;
-                    if (q < rows_per_lane) wsm[lane + 32 * q] = row < P.m ? loss_prime(P.S, rv[q], P.aux[row]) : 0.0;
-                }
+            for (int q = 0; q < rows_per_lane; ++q) {
+                const int i = lane + 32 * q;
+                const long long row = r0 + i;
+                wsm[i] = row < P.m ? loss_prime(P.S, rs[i], P.aux[row]) : 0.0;
             }
-            // pass 1: A_{b,p}^T w from shared memory and publish -- never waits on TMEM,
-            // so a block's completion is not held back by the TMEM ring
+            __syncwarp();
+            // pass 1: A_{b,p}^T w from shared memory
             for (int g0 = 0; g0 < Bmax; g0 += 16) {
                 const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;  // valid smem columns in group
                 double acc[16];
@@ -417,11 +411,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const double colsum = transpose_reduce16(acc, lane);
                 if (lane < ncg && g0 + lane < nc) {
                     if (P.deterministic) P.part[p * Bmax + g0 + lane] = colsum;
-                    else atomicAdd(&P.gacc[slot * Bmax + g0 + lane], colsum);
+                    else atomicAdd(&gacc[g0 + lane], colsum);
                 }
             }
-            __syncwarp();
-            if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);  // partials before the count
             ASY_TRACE(P, md.t, 3);
             // pass 2: park the panel in TMEM (smem -> regs -> tcgen05.st) and free the stage
             if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
@@ -444,6 +436,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);  // panel now lives in TMEM: free the smem stage
+            // publish: the partials' red.adds were issued before pass 2, so this release rarely waits
+            if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);
             // hand the TMEM slot to the axpy warp of this pair
             tmem_wait_st();
             tc_fence_before();
@@ -458,42 +452,71 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         const int d = warp;
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
         double* dv = dxs + d * Bpad;
+        long long pend_slot = -1, pend_b = -1;  // completion of the previous panel, issued late
+        auto complete = [&]() {
+            if (pend_slot >= 0 && lane == 0) {
+                red_add_release_u32(&P.consumed[pend_slot], 1u);  // r red.adds, x/gacc writes before
+                red_add_release_u32(&P.xver[pend_b], 1u);
+            }
+            pend_slot = -1;
+        };
         for (long long j = 0;; ++j) {
             const int ts = (int)(j % TS);
-            mbar_wait(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1));
+            // the previous panel's completion is issued now unless the next panel is already here;
+            // never deferred across a wait (a guard elsewhere may be waiting for it)
+            if (!mbar_test(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1))) {
+                complete();
+                mbar_wait(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1));
+            }
             tc_fence_after();
             const StageMeta md = tmeta[d * TS + ts];
             if (md.t < 0) break;
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
+            const long long use = k / P.slots;
+            const double* gacc = P.gacc + (slot * 2 + (use & 1)) * Bmax;
+            double* gnext = P.gacc + (slot * 2 + ((use + 1) & 1)) * Bmax;
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
+            const long long u = k / P.nblk;
+            const double* xr = (u & 1) ? P.x1 : P.x0;
+            double* xw = (u & 1) ? P.x0 : P.x1;
             ASY_TRACE(P, md.t, 5);
-            // all G partials of sequence k published?
-            if (lane == 0) spin_until_ge_u32(&P.arrive[slot], (unsigned)P.G);
-            ASY_TRACE(P, md.t, 6);
+            // all G partials of sequence k published?  (flush the pending completion before
+            // blocking: a guard that admits this very sequence may be waiting for it)
+            {
+                const unsigned need = (unsigned)((use + 1) * P.G);
+                unsigned ok = 0;
+                if (lane == 0) ok = ld_acquire_u32(&P.arrive[slot]) >= need;
+                ok = __shfl_sync(0xffffffffu, ok, 0);
+                if (!ok) {
+                    complete();
+                    if (lane == 0) spin_until_ge_u32(&P.arrive[slot], need);
+                }
+            }
             __syncwarp();
+            ASY_TRACE(P, md.t, 6);
             // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block
-            double xn[(128 + 31) / 32];
             bool nz = false;
 #pragma unroll
             for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
                 const int c = lane + 32 * s4;
                 double dd = 0.0;
-                xn[s4] = 0.0;
                 if (c < nc) {
                     double g;
                     if (P.deterministic) {
                         g = 0.0;
                         for (long long q = 0; q < P.G; ++q) g += ld_relaxed_f64(&P.part[q * Bmax + c]);
                     } else {
-                        g = ld_relaxed_f64(&P.gacc[slot * Bmax + c]);
+                        g = ld_relaxed_f64(&gacc[c]);
+                        gnext[c] = 0.0;  // the slot's next user accumulates into the other half
                     }
                     const long long jj = c0 + c;
-                    const double y = ld_relaxed_f64(&P.x[jj]);
+                    const double y = xr[jj];
                     const double xh = best_response(P.S, g, y, P.tau[jj], jj);
-                    xn[s4] = y + P.gamma * (xh - y);
-                    dd = xn[s4] - y;
+                    const double xn = y + P.gamma * (xh - y);
+                    xw[jj] = xn;  // every panel writes the same value
+                    dd = xn - y;
                 }
                 if (c < Bpad) dv[c] = dd;
                 nz |= dd != 0.0;
@@ -504,53 +527,34 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
             if (nz) {
 #pragma unroll 1
-                for (int q = 0; q < kMaxRowsPerLane; ++q) {
-                    if (q < rows_per_lane) {
-                        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-                        for (int c8 = 0; c8 < Bpad; c8 += 8) {
-                            uint32_t u[16];
-                            tmem_ld8(tslot + (uint32_t)(q * cols_per_row + 2 * c8), u);
-                            tmem_wait_ld();
+                for (int q = 0; q < rows_per_lane; ++q) {
+                    double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int c0p = 0; c0p < Bpad; c0p += 32) {
+                        const int nch = (Bpad - c0p) < 32 ? (Bpad - c0p) / 8 : 4;
+                        uint32_t u[64];
+                        const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * c0p);
 #pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                acc4[i & 3] = fma(u2d(u[2 * i], u[2 * i + 1]), dv[c8 + i], acc4[i & 3]);
-                        }
-                        const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-                        const long long row = r0 + lane + 32 * q;
-                        if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
+                        for (int s8 = 0; s8 < 4; ++s8)
+                            if (s8 < nch) tmem_ld8(trow + 16 * s8, u + 16 * s8);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < 8 * nch) acc4[i & 3] = fma(u2d(u[2 * i], u[2 * i + 1]), dv[c0p + i], acc4[i & 3]);
                     }
+                    const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+                    const long long row = r0 + lane + 32 * q;
+                    if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
                 }
             }
             tc_fence_before();
             __syncwarp();
             ASY_TRACE(P, md.t, 7);
-            unsigned last = 0;
-            if (lane == 0) {
-                mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free
-                // reads of gacc/x and the red.adds above are performed before the count moves
-                last = atom_add_acqrel_u32(&P.consumed[slot], 1u) == (unsigned)(P.G - 1);
-            }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                // last panel of sequence k: write x_b, recycle the slot, publish completion
-#pragma unroll
-                for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
-                    const int c = lane + 32 * s4;
-                    if (c < nc) {
-                        P.x[c0 + c] = xn[s4];
-                        if (!P.deterministic) P.gacc[slot * Bmax + c] = 0.0;
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    P.arrive[slot] = 0u;
-                    P.consumed[slot] = 0u;
-                    __threadfence();
-                    st_release_u32(&P.xver[b], (unsigned)(k / P.nblk) + 1u);
-                    st_release_s64(&P.done[slot], k);
-                }
-            }
+            if (lane == 0) mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free
+            complete();  // the one before this panel (if the wait above did not flush it)
+            pend_slot = slot;
+            pend_b = b;
         }
+        complete();
     }
     tc_fence_before();
     __syncthreads();
