@@ -448,7 +448,10 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
     }
 
     // ---- vectors
-    TRY(copy_in(h, h->b, p->b, sizeof(double) * p->m, cm));
+    TRY(dev_alloc(h, h->b, sizeof(double) * (p->m + 32)));  // padded: bulk copies of b rows
+    CK(cudaMemsetAsync(h->b.p, 0, sizeof(double) * (p->m + 32), h->stream));
+    CK(cudaMemcpyAsync(h->b.p, p->b, sizeof(double) * p->m,
+                       cm == ASY_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
     TRY(copy_in(h, h->tau, p->tau, sizeof(double) * p->n, cm));
     if (p->lo) {
         TRY(copy_in(h, h->lo, p->lo, sizeof(double) * p->n, cm));
@@ -555,17 +558,18 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int64_t G = (h->m + R - 1) / R;
     const int64_t cols_per_slot = (R / 32) * 2 * Bpad;
     const int TS = (int)std::min<int64_t>(kMaxTmemSlots, 512 / cols_per_slot);
-    const size_t panel = sizeof(double) * R * (B + 1);  // A tile + residual rows
+    const size_t panel = sizeof(double) * R * (B + 2);  // A tile + residual rows + rows of b / y
     const size_t fixed = sizeof(double) * kPairs * (Bpad + R) + sizeof(StageMeta) * kPairs * TS +
                          sizeof(uint64_t) * 2 * kPairs * TS + (sizeof(StageMeta) + 2 * sizeof(uint64_t)) * kQueue +
-                         64;
+                         64 + 16;
     int NS = sp->stages;
     if (NS <= 0) {
         NS = (int)((200 * 1024 - fixed) / (panel + sizeof(StageMeta) + 2 * sizeof(uint64_t)));
         NS = std::min(16, NS);
     }
-    NS = NS / kPairs * kPairs;
-    if (NS < kPairs) return h->fail(ASY_ERR_INVALID, "panel too large: need at least %d stages", kPairs);
+    NS = NS / kPairs * kPairs;  // pair d owns stages d (mod kPairs); one stage per pair in flight
+    NS = std::min(NS, kPairs);  // (more would let an unpublished panel wait behind a TMEM slot)
+    if (NS < kPairs) return h->fail(ASY_ERR_INVALID, "panel too large: need %d stages", kPairs);
     const size_t smem = panel * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t));
     if (smem > 227 * 1024)
         return h->fail(ASY_ERR_INVALID, "panel_rows*block_size*stages too large for shared memory (%zu B)", smem);

@@ -11,7 +11,7 @@
 // residual).  A panel is read from HBM exactly once.
 //
 // Warp roles.  Four "pairs" d = 0..3; pair d owns smem stages st = d (mod 4)
-// and the TMEM lane quarter [32d, 32d+32):
+// and the TMEM lane quarter [32d, 32d+32) with a ring of TMEM slots in it:
 //   warp 9 (lane 0)   scheduler: claims subtasks in batches of kClaim from the
 //                     counter, checks the guards below (acquire) and queues
 //                     the admitted subtasks in shared memory;
@@ -143,6 +143,9 @@ __device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint
                  : "memory");
 }
 
+__device__ __forceinline__ void red_add_u32(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add_release_u32(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     const int R = (int)P.R;
     const int Bmax = P.Bmax, Bpad = P.Bpad;
     const size_t PANEL = (size_t)R * Bmax;   // doubles of A per stage
-    const size_t STAGE = PANEL + R;          // + the R residual rows
+    const size_t STAGE = PANEL + 2 * R;      // + the R residual rows + the R rows of b / y
     double* stages = reinterpret_cast<double*>(smem_raw);                       // NS * STAGE
     double* dxs = stages + NS * STAGE;                                          // kPairs * Bpad
     double* wbuf = dxs + kPairs * Bpad;                                         // kPairs * R
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     uint64_t* qfull = tempty + kPairs * TS;                                     // kQueue
     uint64_t* qempty = qfull + kQueue;                                          // kQueue
     uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + kQueue);
+    unsigned* dot_ticket = tmem_base_s + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kProducerWarp) {
@@ -247,6 +251,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
             for (int s = 0; s < kPairs * TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 1); }
             for (int s = 0; s < kQueue; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qempty[s], 1); }
+            *dot_ticket = 0u;
             mbar_fence_init();
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
         }
@@ -291,9 +296,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const long long nr = (P.m - r0) < R ? (P.m - r0) : R;
                 const uint32_t rbytes = (uint32_t)(((nr + 1) & ~1ll) * 8);
                 double* dst = stages + st * STAGE;
-                mbar_arrive_expect_tx(&full[st], box_bytes + rbytes);
+                mbar_arrive_expect_tx(&full[st], box_bytes + 2 * rbytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
                 bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
+                bulk_g2s_nohint(dst + PANEL + R, P.aux + r0, rbytes, &full[st]);
             }
         }
         __syncwarp();
@@ -364,12 +370,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
         double* wsm = wbuf + d * R;
         for (long long j = 0;; ++j) {
-            const long long it = j * kPairs + d;
+            const long long it = j * kPairs + d;  // static: pair d owns stages d (mod kPairs)
             const int st = (int)(it % NS);
             const int ts = (int)(j % TS);
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
             const StageMeta md = meta[st];
             if (md.t < 0) {
+                if (lane == 0) mbar_arrive(&empty[st]);  // the producer may reuse the stage for another marker
                 if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
                 if (lane == 0) {
                     tmeta[d * TS + ts].t = -1;
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             for (int q = 0; q < rows_per_lane; ++q) {
                 const int i = lane + 32 * q;
                 const long long row = r0 + i;
-                wsm[i] = row < P.m ? loss_prime(P.S, rs[i], P.aux[row]) : 0.0;
+                wsm[i] = row < P.m ? loss_prime(P.S, rs[i], rs[R + i]) : 0.0;
             }
             __syncwarp();
             // pass 1: A_{b,p}^T w from shared memory
@@ -455,8 +462,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         long long pend_slot = -1, pend_b = -1;  // completion of the previous panel, issued late
         auto complete = [&]() {
             if (pend_slot >= 0 && lane == 0) {
-                red_add_release_u32(&P.consumed[pend_slot], 1u);  // r red.adds, x/gacc writes before
-                red_add_release_u32(&P.xver[pend_b], 1u);
+                fence_acqrel_gpu();  // r red.adds, x / accumulator writes before the counts (one membar)
+                red_add_u32(&P.consumed[pend_slot], 1u);
+                red_add_u32(&P.xver[pend_b], 1u);
             }
             pend_slot = -1;
         };
@@ -482,6 +490,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const double* xr = (u & 1) ? P.x1 : P.x0;
             double* xw = (u & 1) ? P.x0 : P.x1;
             ASY_TRACE(P, md.t, 5);
+            // x_b (previous epoch, final by the D4 guard) and tau do not depend on the arrivals
+            double ypre[(128 + 31) / 32], tpre[(128 + 31) / 32];
+#pragma unroll
+            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+                const int c = lane + 32 * s4;
+                ypre[s4] = c < nc ? xr[c0 + c] : 0.0;
+                tpre[s4] = c < nc ? P.tau[c0 + c] : 1.0;
+            }
             // all G partials of sequence k published?  (flush the pending completion before
             // blocking: a guard that admits this very sequence may be waiting for it)
             {
@@ -512,8 +528,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         gnext[c] = 0.0;  // the slot's next user accumulates into the other half
                     }
                     const long long jj = c0 + c;
-                    const double y = xr[jj];
-                    const double xh = best_response(P.S, g, y, P.tau[jj], jj);
+                    const double y = ypre[s4];
+                    const double xh = best_response(P.S, g, y, tpre[s4], jj);
                     const double xn = y + P.gamma * (xh - y);
                     xw[jj] = xn;  // every panel writes the same value
                     dd = xn - y;
@@ -529,17 +545,22 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll 1
                 for (int q = 0; q < rows_per_lane; ++q) {
                     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-                    for (int c0p = 0; c0p < Bpad; c0p += 32) {
-                        const int nch = (Bpad - c0p) < 32 ? (Bpad - c0p) / 8 : 4;
-                        uint32_t u[64];
-                        const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * c0p);
-#pragma unroll
-                        for (int s8 = 0; s8 < 4; ++s8)
-                            if (s8 < nch) tmem_ld8(trow + 16 * s8, u + 16 * s8);
+                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row);
+#pragma unroll 1
+                    for (int c8 = 0; c8 < Bpad; c8 += 8) {
+                        uint32_t u[16];
+                        tmem_ld8(trow + 2 * c8, u);
+                        const double2* d2 = reinterpret_cast<const double2*>(dv + c8);  // LDS.128 broadcast
+                        const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
                         tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < 8 * nch) acc4[i & 3] = fma(u2d(u[2 * i], u[2 * i + 1]), dv[c0p + i], acc4[i & 3]);
+                        acc4[0] = fma(u2d(u[0], u[1]), da.x, acc4[0]);
+                        acc4[1] = fma(u2d(u[2], u[3]), da.y, acc4[1]);
+                        acc4[2] = fma(u2d(u[4], u[5]), db.x, acc4[2]);
+                        acc4[3] = fma(u2d(u[6], u[7]), db.y, acc4[3]);
+                        acc4[0] = fma(u2d(u[8], u[9]), dc.x, acc4[0]);
+                        acc4[1] = fma(u2d(u[10], u[11]), dc.y, acc4[1]);
+                        acc4[2] = fma(u2d(u[12], u[13]), dd2.x, acc4[2]);
+                        acc4[3] = fma(u2d(u[14], u[15]), dd2.y, acc4[3]);
                     }
                     const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
                     const long long row = r0 + lane + 32 * q;
