@@ -35,7 +35,7 @@ TARGET = 1e-6
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
@@ -89,7 +89,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -242,6 +242,8 @@ def run_ours(args, rank, world, local):
     hbm_peak, peak_kind = peaks()
     achieved = bytes_per_sweep(P) * sweeps / (kernel_ms * 1e-3) / 1e9
     traffic = traffic_for(P)
+    if traffic is not None:
+        traffic = traffic * args.check_every  # per launch (one launch = check_every sweeps), like `achieved`
     last_stat = res[-1][4]
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
