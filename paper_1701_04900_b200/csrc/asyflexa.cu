@@ -540,8 +540,8 @@ static EncodeTiledFn encode_tiled() {
 }
 
 struct DenseGeom {
-    int64_t R, G;
-    int NS, TS, Bpad, grid;
+    int64_t R, G, delay;
+    int Bpad, grid, use_tmem;
     size_t smem;
 };
 
@@ -552,37 +552,30 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     if (R <= 0) R = 4096 / B;                       // ~32 KB panels
     R = (R + 31) / 32 * 32;
     R = std::max<int64_t>(32, std::min<int64_t>(R, 256));
-    while (R > 32 && (R / 32) * 2 * Bpad > 512) R -= 32;  // one panel must fit a TMEM lane quarter
     const int64_t mr = (h->m + 31) / 32 * 32;
     if (R > mr) R = mr;
     const int64_t G = (h->m + R - 1) / R;
-    const int64_t cols_per_slot = (R / 32) * 2 * Bpad;
-    const int TS = (int)std::min<int64_t>(kMaxTmemSlots, 512 / cols_per_slot);
-    const size_t panel = sizeof(double) * R * (B + 2);  // A tile + residual rows + rows of b / y
-    const size_t fixed = sizeof(double) * kPairs * (Bpad + R) + sizeof(StageMeta) * kPairs * TS +
-                         sizeof(uint64_t) * 2 * kPairs * TS + (sizeof(StageMeta) + 2 * sizeof(uint64_t)) * kQueue +
-                         64 + 16;
-    int NS = sp->stages;
-    if (NS <= 0) {
-        NS = (int)((200 * 1024 - fixed) / (panel + sizeof(StageMeta) + 2 * sizeof(uint64_t)));
-        NS = std::min(16, NS);
-    }
-    NS = NS / kPairs * kPairs;  // pair d owns stages d (mod kPairs); one stage per pair in flight
-    NS = std::min(NS, kPairs);  // (more would let an unpublished panel wait behind a TMEM slot)
-    if (NS < kPairs) return h->fail(ASY_ERR_INVALID, "panel too large: need %d stages", kPairs);
-    const size_t smem = panel * NS + fixed + NS * (sizeof(StageMeta) + 2 * sizeof(uint64_t));
+    const int use_tmem = (R / 32) * 2 * Bpad <= kSlotCols;
+    constexpr int NAX = kPairs * kAxpyPerPair;
+    const size_t smem = sizeof(double) * (kPairs * (R * B + 2 * R) + NAX * Bpad + kPairs * R) +
+                        sizeof(StageMeta) * (kPairs + kQueue) + sizeof(Handoff) * NAX * kRing +
+                        sizeof(uint64_t) * (2 * kPairs + 2 * kQueue + 2 * NAX * kRing) + sizeof(unsigned) * (NAX + 1) +
+                        64;
     if (smem > 227 * 1024)
-        return h->fail(ASY_ERR_INVALID, "panel_rows*block_size*stages too large for shared memory (%zu B)", smem);
+        return h->fail(ASY_ERR_INVALID, "panel_rows*block_size too large for shared memory (%zu B)", smem);
     CK(cudaFuncSetAttribute(dense_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_async_kernel, kDenseThreads, smem));
     if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense async kernel does not fit on an SM");
     int grid = h->sms;  // one CTA per SM: it owns the SM's whole TMEM (512 columns)
     // enough workers to keep ~2x the delay window of panels in flight, never more
-    const int64_t want = (2 * (delay + 1) * G + NS - 1) / NS;
+    const int64_t want = (2 * (delay + 1) * G + kPairs - 1) / kPairs;
     if (want < grid) grid = (int)std::max<int64_t>(1, want);
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
-    g->R = R; g->G = G; g->NS = NS; g->TS = TS; g->Bpad = (int)Bpad; g->grid = grid; g->smem = smem;
+    // blocks in flight are capped so that a block's panels never fill an axpy warp's hand-off ring
+    const int64_t cap = std::max<int64_t>(0, (int64_t)kRing * NAX * grid / (4 * G) - 1);
+    g->delay = std::min<int64_t>(delay, cap);
+    g->R = R; g->G = G; g->Bpad = (int)Bpad; g->grid = grid; g->smem = smem; g->use_tmem = use_tmem;
     return ASY_OK;
 }
 
@@ -612,15 +605,19 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk));
 
     DenseAsyncParams P{};
-    P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G;
+    P.A = P_<double>(h->A); P.lda = h->lda;
+    // a block whose panels exceed ~half the machine's TMEM slots will be partly re-read: keep it in L2
+    P.keep_in_l2 = !geo.use_tmem || G * 2 > (int64_t)geo.grid * kPairs * kTmemSlots;
+    P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G; P.use_tmem = geo.use_tmem;
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
     P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
+    delay = geo.delay;
     P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
     P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
     P.xver = P_<unsigned>(h->ver);
-    P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad; P.stages = geo.NS; P.tslots = geo.TS;
+    P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad;
 
     // debug trace (env ASY_TRACE=<subtasks>, ASY_TRACE_FILE=<path>): globaltimer stamps per subtask
     const char* tr = getenv("ASY_TRACE");

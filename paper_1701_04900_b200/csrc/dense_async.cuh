@@ -6,40 +6,42 @@
 // where sequence k updates block b = schedule(k) (S.1) and panel p covers
 // rows [p*R, p*R+R) of that block's columns A_b: an R x B tile loaded by one
 // 2-D TMA (cp.async.bulk.tensor, OOB rows/columns zero-filled) into a stage of
-// an NS-deep shared-memory ring, together with the R residual rows it needs
-// (1-D bulk copy, read at issue time: the inconsistent read of the shared
-// residual).  A panel is read from HBM exactly once.
+// a 4-deep shared-memory ring, together with the R residual rows it needs and
+// the R rows of b / y (1-D bulk copies; the residual is read at issue time:
+// the inconsistent read of the shared residual).
 //
-// Warp roles.  Four "pairs" d = 0..3; pair d owns smem stages st = d (mod 4)
-// and the TMEM lane quarter [32d, 32d+32) with a ring of TMEM slots in it:
-//   warp 9 (lane 0)   scheduler: claims subtasks in batches of kClaim from the
-//                     counter, checks the guards below (acquire) and queues
-//                     the admitted subtasks in shared memory;
-//   warp 8 (lane 0)   producer: pops the queue, arms the stage mbarrier and
-//                     issues the two bulk copies;
-//   warp 4+d  (dot)   w = phi'(r) on the panel rows, A_{b,p}^T w straight from
+// Warp roles.  Four "pairs" q = 0..3; pair q owns smem stage q and the TMEM
+// lane quarter [32q, 32q+32), split into two 256-column panel slots:
+//   warp 13 (lane 0)  scheduler: claims subtasks in batches of kClaim from the
+//                     counter, checks the guards below (acquire) and queues the
+//                     admitted subtasks in shared memory;
+//   warp 12 (lane 0)  producer: pops the queue, arms the stage mbarrier and
+//                     issues the three bulk copies;
+//   warp 4+q  (dot)   w = phi'(r) on the panel rows, A_{b,p}^T w straight from
 //                     shared memory (lane = rows, 16 column accumulators,
 //                     butterfly transpose-reduction), red.add into the
-//                     sequence's accumulator; parks the panel in TMEM (smem ->
-//                     registers -> tcgen05.st), frees the smem stage and only
-//                     then release-adds the sequence's arrival counter (the
-//                     partials' red.adds have drained meanwhile);
-//   warp d    (axpy)  waits until all G panels of its sequence arrived, solves
-//                     the block subproblem (Eq. 2, closed form) and applies
-//                     (S.4) -- every panel of the block does this redundantly
-//                     and bit-identically, writing the new x_b into the other
-//                     half of a double-buffered x -- reads its panel back from
-//                     TMEM (tcgen05.ld), pushes A_{b,p} dx_b into r (red.add)
-//                     and frees the TMEM slot; its completion (release-adds of
-//                     the sequence and block counters) is issued one panel
-//                     later, overlapping the next block's wait.
+//                     sequence's accumulator; if the TMEM slot of the axpy warp
+//                     that will take the panel is free, parks the panel there
+//                     (smem -> registers -> tcgen05.st), otherwise marks it
+//                     "re-read"; frees the smem stage, release-adds the
+//                     sequence's arrival counter and queues a hand-off note.
+//                     It never waits on TMEM or on a block's completion, so
+//                     every loaded panel is published (no deadlock however many
+//                     panels a block has);
+//   warps q, 8+q      (axpy, alternating hand-offs of pair q): wait until all G
+//                     panels of the sequence arrived, solve the block
+//                     subproblem (Eq. 2, closed form) and (S.4) -- every panel
+//                     of the block does it redundantly and bit-identically,
+//                     writing the new x_b into the other half of a
+//                     double-buffered x -- read the panel back (TMEM, or A
+//                     again from L2 when it was not parked), push A_{b,p} dx_b
+//                     into r (red.add), free the TMEM slot; completion
+//                     (release-adds of the sequence and block counters) is
+//                     issued one panel later unless the warp would block.
 // No "last panel" role exists: all counters are monotonic (sequence k owns
 // arrival / completion counts ((k/S)+1)*G in slot k mod S), the accumulator is
 // double-buffered per slot use and zeroed by the next use's consumers, and x
 // is double-buffered per epoch.
-// TMEM (256 KB/SM) holds the panels that wait for their block's dx, so the
-// 227 KB of shared memory only covers load latency: in-flight capacity per SM
-// is smem + TMEM.
 // Guards, checked by the scheduler before a panel is loaded (all point to
 // strictly older sequences -> deadlock free with co-resident CTAs):
 //   * D4 freshness [PAPER.md:233]: block b is not read before its previous
@@ -57,22 +59,28 @@
 namespace asy {
 
 constexpr int kPairs = 4;
-constexpr int kProducerWarp = 2 * kPairs;
-constexpr int kSchedWarp = 2 * kPairs + 1;
-constexpr int kDenseThreads = 32 * (2 * kPairs + 2);
-constexpr int kQueue = 4;           // scheduler -> producer queue depth
-constexpr int kMaxRowsPerLane = 8;  // R <= 256 (one TMA box per panel)
-constexpr int kMaxTmemSlots = 8;
-constexpr int kClaim = 4;           // subtasks claimed per atomic
+constexpr int kAxpyPerPair = 1;
+constexpr int kTmemSlots = 2;        // parked panels per pair (TMEM lane quarter = 2 x 256 columns)
+constexpr int kProducerWarp = 8;
+constexpr int kSchedWarp = 9;
+constexpr int kDenseThreads = 32 * 10;
+constexpr int kQueue = 4;            // scheduler -> producer queue depth
+constexpr int kRing = 64;            // hand-off notes per axpy warp
+constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
+constexpr int kClaim = 4;            // subtasks claimed per atomic
+constexpr int kSlotCols = 256;       // TMEM columns per parked panel
+constexpr unsigned long long kParkWaitNs = 20000;  // max wait for a TMEM slot before re-reading
 
 struct DenseAsyncParams {
+    const double* A;  // for re-reads of panels that were not parked in TMEM
+    int64_t lda;
     int64_t m, n;
     int64_t B;      // block size
     int64_t nblk;   // number of blocks
     int64_t R;      // panel rows (multiple of 32, <= 256) = TMA box rows
     int64_t G;      // panels per block
     double* r;      // shared residual (LS: Ax-b, logistic: Ax); >= m+32 entries
-    const double* aux;  // b (LS) or y (logistic)
+    const double* aux;  // b (LS) or y (logistic); >= m+32 entries
     double* x0;     // x buffer read in even local epochs (written in odd ones)
     double* x1;     // x buffer read in odd local epochs
     const double* tau;
@@ -84,6 +92,8 @@ struct DenseAsyncParams {
     int64_t T;        // subtasks in this launch = K*G
     int64_t delay;    // bounded delay window (>= 0)
     int deterministic;
+    int use_tmem;     // park panels in TMEM when they fit (cols_per_panel <= kSlotCols)
+    int keep_in_l2;   // blocks too large to park: load with L2 evict_normal so re-reads hit L2
     // synchronisation state (initialised by dense_async_init)
     unsigned long long* counter;
     double* gacc;        // [S][2][Bmax] accumulated A_b^T w; sequence k uses [k mod S][(k/S) & 1]
@@ -94,8 +104,6 @@ struct DenseAsyncParams {
     int64_t slots;       // power of two
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
-    int32_t stages;      // multiple of kPairs
-    int32_t tslots;      // TMEM slots per pair
     unsigned long long* trace;  // optional [trace_n][8] globaltimer stamps (debug; null = off)
     int64_t trace_n;
 };
@@ -115,6 +123,11 @@ struct StageMeta {
     long long t, k, b, p;
 };
 
+struct Handoff {
+    StageMeta md;
+    int parked;   // 1 + TMEM slot of the parked panel; 0: re-read A from global
+    int pad;
+};
 
 __global__ void dense_async_init(DenseAsyncParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -220,38 +233,47 @@ __device__ __forceinline__ double transpose_reduce16(double (&v)[16], int lane) 
     return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
 }
 
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const int NS = P.stages;
-    const int TS = P.tslots;
+    constexpr int NS = kPairs;               // one stage per pair
+    constexpr int NAX = kPairs * kAxpyPerPair;
     const int R = (int)P.R;
     const int Bmax = P.Bmax, Bpad = P.Bpad;
     const size_t PANEL = (size_t)R * Bmax;   // doubles of A per stage
     const size_t STAGE = PANEL + 2 * R;      // + the R residual rows + the R rows of b / y
     double* stages = reinterpret_cast<double*>(smem_raw);                       // NS * STAGE
-    double* dxs = stages + NS * STAGE;                                          // kPairs * Bpad
-    double* wbuf = dxs + kPairs * Bpad;                                         // kPairs * R
+    double* dxs = stages + NS * STAGE;                                          // NAX * Bpad
+    double* wbuf = dxs + NAX * Bpad;                                            // kPairs * R
     StageMeta* meta = reinterpret_cast<StageMeta*>(wbuf + kPairs * R);         // NS
-    StageMeta* tmeta = meta + NS;                                               // kPairs * TS
-    StageMeta* queue = tmeta + kPairs * TS;                                     // kQueue
-    uint64_t* full = reinterpret_cast<uint64_t*>(queue + kQueue);               // NS
+    StageMeta* queue = meta + NS;                                               // kQueue
+    Handoff* ring = reinterpret_cast<Handoff*>(queue + kQueue);                 // NAX * kRing
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NAX * kRing);           // NS
     uint64_t* empty = full + NS;                                                // NS
-    uint64_t* tfull = empty + NS;                                               // kPairs * TS
-    uint64_t* tempty = tfull + kPairs * TS;                                     // kPairs * TS
-    uint64_t* qfull = tempty + kPairs * TS;                                     // kQueue
+    uint64_t* qfull = empty + NS;                                               // kQueue
     uint64_t* qempty = qfull + kQueue;                                          // kQueue
-    uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + kQueue);
-    unsigned* dot_ticket = tmem_base_s + 1;
+    uint64_t* rfull = qempty + kQueue;                                          // NAX * kRing
+    uint64_t* rempty = rfull + NAX * kRing;                                     // NAX * kRing
+    unsigned* tm_done = reinterpret_cast<unsigned*>(rempty + NAX * kRing);      // NAX
+    uint32_t* tmem_base_s = tm_done + NAX;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == kProducerWarp) {
         tmem_alloc_512(tmem_base_s);
         if (lane == 0) {
             for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-            for (int s = 0; s < kPairs * TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 1); }
             for (int s = 0; s < kQueue; ++s) { mbar_init(&qfull[s], 1); mbar_init(&qempty[s], 1); }
-            *dot_ticket = 0u;
+            for (int s = 0; s < NAX * kRing; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
+            for (int s = 0; s < NAX; ++s) tm_done[s] = 0u;
             mbar_fence_init();
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
         }
@@ -261,14 +283,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_s;
     const int rows_per_lane = R / 32;
-    const int cols_per_row = 2 * Bpad;                      // b32 TMEM columns per panel row
-    const int cols_per_slot = rows_per_lane * cols_per_row;
+    const int cols_per_row = 2 * Bpad;  // b32 TMEM columns per panel row
 
     if (warp == kProducerWarp) {
         // ------------------------------------------------------------------ producer
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
             const uint32_t box_bytes = (uint32_t)(PANEL * 8);
+            const uint64_t pol = P.keep_in_l2 ? policy_evict_normal() : policy_evict_first();
             int ends = 0;
             long long qi = 0;
             for (long long it = 0;; ++it) {
@@ -318,8 +339,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const long long tb = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
                 if (tb >= P.T) break;
                 StageMeta e[kClaim];
-                unsigned xv[kClaim];
-                long long ds[kClaim], dw[kClaim];
+                unsigned xv[kClaim], cs[kClaim], cw[kClaim];
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long t = tb + i;
@@ -330,7 +350,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     ASY_TRACE(P, t, 0);
                 }
                 // guards: all loads in flight at once
-                unsigned cs[kClaim], cw[kClaim];
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long k = e[i].k, kd = k - P.delay - 1;
@@ -364,23 +383,31 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             push(end);
         }
         __syncwarp();
-    } else if (warp >= kPairs) {
+    } else if (warp >= kPairs && warp < 2 * kPairs) {
         // ------------------------------------------------------------------ dot warps
-        const int d = warp - kPairs;
-        const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
-        double* wsm = wbuf + d * R;
+        const int q = warp - kPairs;
+        const uint32_t tlane = tmem_base + ((uint32_t)(32 * q) << 16);
+        double* wsm = wbuf + q * R;
+        unsigned tm_used = 0u;  // panels parked by this pair so far (slot = tm_used % kTmemSlots)
         for (long long j = 0;; ++j) {
-            const long long it = j * kPairs + d;  // static: pair d owns stages d (mod kPairs)
+            const long long it = j * kPairs + q;  // pair q owns stage q
             const int st = (int)(it % NS);
-            const int ts = (int)(j % TS);
+            const int h = 0;                                   // one axpy warp per pair
+            const int ax = q;                                  // its warp id
+            const long long e = j;                             // its ring position
+            const int rs = (int)(e % kRing);
+            Handoff* ho = &ring[(q * kAxpyPerPair + h) * kRing + rs];
+            uint64_t* rf = &rfull[(q * kAxpyPerPair + h) * kRing + rs];
+            uint64_t* re = &rempty[(q * kAxpyPerPair + h) * kRing + rs];
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
             const StageMeta md = meta[st];
             if (md.t < 0) {
-                if (lane == 0) mbar_arrive(&empty[st]);  // the producer may reuse the stage for another marker
-                if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
+                if (lane == 0) mbar_arrive(&empty[st]);
+                // end marker for the pair's axpy warp
+                if (e >= kRing) mbar_wait(re, (uint32_t)(((e / kRing) - 1) & 1));
                 if (lane == 0) {
-                    tmeta[d * TS + ts].t = -1;
-                    mbar_arrive(&tfull[d * TS + ts]);
+                    ho->md.t = -1;
+                    mbar_arrive(rf);
                 }
                 break;
             }
@@ -390,14 +417,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const double* pan = stages + st * STAGE;
-            const double* rs = pan + PANEL;
+            const double* rsm = pan + PANEL;
             ASY_TRACE(P, md.t, 2);
-            // w = phi'(r) on the panel rows (residual rows arrived with the panel)
+            // w = phi'(r) on the panel rows (residual and b / y rows arrived with the panel)
             const long long r0 = p * R;
-            for (int q = 0; q < rows_per_lane; ++q) {
-                const int i = lane + 32 * q;
-                const long long row = r0 + i;
-                wsm[i] = row < P.m ? loss_prime(P.S, rs[i], rs[R + i]) : 0.0;
+            for (int qq = 0; qq < rows_per_lane; ++qq) {
+                const int i = lane + 32 * qq;
+                wsm[i] = (r0 + i) < P.m ? loss_prime(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
             __syncwarp();
             // pass 1: A_{b,p}^T w from shared memory
@@ -407,8 +433,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 16; ++c) acc[c] = 0.0;
 #pragma unroll 2
-                for (int q = 0; q < rows_per_lane; ++q) {
-                    const int i = lane + 32 * q;
+                for (int qq = 0; qq < rows_per_lane; ++qq) {
+                    const int i = lane + 32 * qq;
                     const double w = wsm[i];
                     const double* a = pan + (size_t)g0 * R + i;
 #pragma unroll
@@ -422,43 +448,69 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             ASY_TRACE(P, md.t, 3);
-            // pass 2: park the panel in TMEM (smem -> regs -> tcgen05.st) and free the stage
-            if (j >= TS) mbar_wait(&tempty[d * TS + ts], (uint32_t)(((j / TS) - 1) & 1));
-            tc_fence_after();
-            ASY_TRACE(P, md.t, 4);
-            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
-            for (int g0 = 0; g0 < Bpad; g0 += 16) {
-                const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;
-                const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;
-#pragma unroll 1
-                for (int q = 0; q < rows_per_lane; ++q) {
-                    const double* a = pan + (size_t)g0 * R + lane + 32 * q;
-                    double v[16];
-#pragma unroll
-                    for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
-                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row + 2 * g0);
-                    tmem_st8(trow, v);
-                    if (npg > 8) tmem_st8(trow + 16, v + 8);
+            // park in the axpy warp's TMEM slot if it is free; otherwise the axpy re-reads A
+            // (bounded wait: holding the stage indefinitely could hold back a block whose
+            // panel is queued behind it, so after kParkWaitNs the panel is left in HBM/L2)
+            int parked = 0;
+            if (P.use_tmem) {
+                unsigned ok = 0;
+                if (lane == 0) {
+                    ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                    if (!ok) {
+                        const unsigned long long t0 = gtimer();
+                        do {
+                            __nanosleep(64);
+                            ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                        } while (!ok && gtimer() - t0 < kParkWaitNs);
+                    }
                 }
+                parked = __shfl_sync(0xffffffffu, ok, 0);
+            }
+            ASY_TRACE(P, md.t, 4);
+            const int tslot_idx = (int)(tm_used % kTmemSlots);
+            if (parked) {
+                tc_fence_after();
+                const uint32_t tslot = tlane + (uint32_t)(tslot_idx * kSlotCols);
+                for (int g0 = 0; g0 < Bpad; g0 += 16) {
+                    const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;
+                    const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;
+#pragma unroll 1
+                    for (int qq = 0; qq < rows_per_lane; ++qq) {
+                        const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
+                        double v[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
+                        const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
+                        tmem_st8(trow, v);
+                        if (npg > 8) tmem_st8(trow + 16, v + 8);
+                    }
+                }
+                ++tm_used;
+                tmem_wait_st();
+                tc_fence_before();
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);  // panel now lives in TMEM: free the smem stage
-            // publish: the partials' red.adds were issued before pass 2, so this release rarely waits
+            // publish (the partials' red.adds drained during the parking pass)
             if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);
-            // hand the TMEM slot to the axpy warp of this pair
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
+            // hand-off note (after publishing: waiting here can never hold back a block)
+            if (e >= kRing) mbar_wait(re, (uint32_t)(((e / kRing) - 1) & 1));
             if (lane == 0) {
-                tmeta[d * TS + ts] = md;
-                mbar_arrive(&tfull[d * TS + ts]);
+                mbar_arrive(&empty[st]);  // smem stage free
+                ho->md = md;
+                ho->parked = parked ? 1 + tslot_idx : 0;
+                mbar_arrive(rf);
             }
         }
     } else {
         // ------------------------------------------------------------------ axpy warps
-        const int d = warp;
-        const uint32_t tlane = tmem_base + ((uint32_t)(32 * d) << 16);
-        double* dv = dxs + d * Bpad;
+        const int q = warp, h = 0;
+        const int ax = warp;
+        const uint32_t tquarter = tmem_base + ((uint32_t)(32 * q) << 16);
+        double* dv = dxs + (q * kAxpyPerPair + h) * Bpad;
+        Handoff* myring = ring + (q * kAxpyPerPair + h) * kRing;
+        uint64_t* myfull = rfull + (q * kAxpyPerPair + h) * kRing;
+        uint64_t* myempty = rempty + (q * kAxpyPerPair + h) * kRing;
+        unsigned tm_fin = 0;
         long long pend_slot = -1, pend_b = -1;  // completion of the previous panel, issued late
         auto complete = [&]() {
             if (pend_slot >= 0 && lane == 0) {
@@ -468,16 +520,18 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             pend_slot = -1;
         };
-        for (long long j = 0;; ++j) {
-            const int ts = (int)(j % TS);
-            // the previous panel's completion is issued now unless the next panel is already here;
+        for (long long e = 0;; ++e) {
+            const int rs = (int)(e % kRing);
+            // the previous panel's completion is issued now unless the next one is already here;
             // never deferred across a wait (a guard elsewhere may be waiting for it)
-            if (!mbar_test(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1))) {
+            if (!mbar_test(&myfull[rs], (uint32_t)((e / kRing) & 1))) {
                 complete();
-                mbar_wait(&tfull[d * TS + ts], (uint32_t)((j / TS) & 1));
+                mbar_wait(&myfull[rs], (uint32_t)((e / kRing) & 1));
             }
-            tc_fence_after();
-            const StageMeta md = tmeta[d * TS + ts];
+            const Handoff hd = myring[rs];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&myempty[rs]);
+            const StageMeta md = hd.md;
             if (md.t < 0) break;
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
@@ -522,7 +576,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     double g;
                     if (P.deterministic) {
                         g = 0.0;
-                        for (long long q = 0; q < P.G; ++q) g += ld_relaxed_f64(&P.part[q * Bmax + c]);
+                        for (long long qq = 0; qq < P.G; ++qq) g += ld_relaxed_f64(&P.part[qq * Bmax + c]);
                     } else {
                         g = ld_relaxed_f64(&gacc[c]);
                         gnext[c] = 0.0;  // the slot's next user accumulates into the other half
@@ -540,38 +594,55 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             nz = __any_sync(0xffffffffu, nz);
             __syncwarp();
             const long long r0 = p * R;
-            const uint32_t tslot = tlane + (uint32_t)(ts * cols_per_slot);
+            if (hd.parked) tc_fence_after();
             if (nz) {
 #pragma unroll 1
-                for (int q = 0; q < rows_per_lane; ++q) {
+                for (int qq = 0; qq < rows_per_lane; ++qq) {
                     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-                    const uint32_t trow = tslot + (uint32_t)(q * cols_per_row);
+                    const long long row = r0 + lane + 32 * qq;
+                    if (hd.parked) {
+                        const uint32_t trow = tquarter + (uint32_t)((hd.parked - 1) * kSlotCols + qq * cols_per_row);
 #pragma unroll 1
-                    for (int c8 = 0; c8 < Bpad; c8 += 8) {
-                        uint32_t u[16];
-                        tmem_ld8(trow + 2 * c8, u);
-                        const double2* d2 = reinterpret_cast<const double2*>(dv + c8);  // LDS.128 broadcast
-                        const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
-                        tmem_wait_ld();
-                        acc4[0] = fma(u2d(u[0], u[1]), da.x, acc4[0]);
-                        acc4[1] = fma(u2d(u[2], u[3]), da.y, acc4[1]);
-                        acc4[2] = fma(u2d(u[4], u[5]), db.x, acc4[2]);
-                        acc4[3] = fma(u2d(u[6], u[7]), db.y, acc4[3]);
-                        acc4[0] = fma(u2d(u[8], u[9]), dc.x, acc4[0]);
-                        acc4[1] = fma(u2d(u[10], u[11]), dc.y, acc4[1]);
-                        acc4[2] = fma(u2d(u[12], u[13]), dd2.x, acc4[2]);
-                        acc4[3] = fma(u2d(u[14], u[15]), dd2.y, acc4[3]);
+                        for (int c8 = 0; c8 < Bpad; c8 += 8) {
+                            uint32_t uu[16];
+                            tmem_ld8(trow + 2 * c8, uu);
+                            const double2* d2 = reinterpret_cast<const double2*>(dv + c8);  // LDS.128 broadcast
+                            const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
+                            tmem_wait_ld();
+                            acc4[0] = fma(u2d(uu[0], uu[1]), da.x, acc4[0]);
+                            acc4[1] = fma(u2d(uu[2], uu[3]), da.y, acc4[1]);
+                            acc4[2] = fma(u2d(uu[4], uu[5]), db.x, acc4[2]);
+                            acc4[3] = fma(u2d(uu[6], uu[7]), db.y, acc4[3]);
+                            acc4[0] = fma(u2d(uu[8], uu[9]), dc.x, acc4[0]);
+                            acc4[1] = fma(u2d(uu[10], uu[11]), dc.y, acc4[1]);
+                            acc4[2] = fma(u2d(uu[12], uu[13]), dd2.x, acc4[2]);
+                            acc4[3] = fma(u2d(uu[14], uu[15]), dd2.y, acc4[3]);
+                        }
+                    } else if (row < P.m) {
+                        // re-read the panel row from global memory (L2, usually)
+                        const double* a = P.A + c0 * P.lda + row;
+#pragma unroll 1
+                        for (int c8 = 0; c8 < nc; c8 += 8) {
+                            double av[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) av[i] = (c8 + i) < nc ? __ldg(a + (c8 + i) * P.lda) : 0.0;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) acc4[i & 3] = fma(av[i], dv[c8 + i], acc4[i & 3]);
+                        }
                     }
                     const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-                    const long long row = r0 + lane + 32 * q;
                     if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
                 }
             }
-            tc_fence_before();
+            if (hd.parked) {
+                tc_fence_before();
+                __syncwarp();
+                ++tm_fin;
+                if (lane == 0) st_release_cta_u32(&tm_done[ax], tm_fin);  // TMEM slot free
+            }
             __syncwarp();
             ASY_TRACE(P, md.t, 7);
-            if (lane == 0) mbar_arrive(&tempty[d * TS + ts]);  // TMEM slot free
-            complete();  // the one before this panel (if the wait above did not flush it)
+            complete();  // the one before this panel (if not flushed above)
             pend_slot = slot;
             pend_b = b;
         }

@@ -9,7 +9,7 @@ tr = tr[ok]
 t0 = tr.min()
 tr = tr - t0
 n = tr.shape[0]
-names = ["claim", "issue", "land", "publish", "tmemslot", "axpystart", "blockdone", "axpydone"]
+names = ["claim", "issue", "land", "partials", "parkdecided", "axpystart", "blockdone", "axpydone"]
 print("subtasks", n, "span us", (tr.max() - tr.min()) / 1e3)
 for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7), (0, 7)]:
     d = (tr[:, b] - tr[:, a]) / 1e3
