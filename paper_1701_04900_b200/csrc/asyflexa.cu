@@ -555,7 +555,8 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int64_t mr = (h->m + 31) / 32 * 32;
     if (R > mr) R = mr;
     const int64_t G = (h->m + R - 1) / R;
-    const int use_tmem = (R / 32) * 2 * Bpad <= kSlotCols;
+    int use_tmem = (R / 32) * 2 * Bpad <= kSlotCols;
+    if (getenv("ASY_NO_TMEM")) use_tmem = 0;  // debug/test: force the re-read path
     constexpr int NAX = kPairs * kAxpyPerPair;
     const size_t smem = sizeof(double) * (kPairs * (R * B + 2 * R) + NAX * Bpad + kPairs * R) +
                         sizeof(StageMeta) * (kPairs + kQueue) + sizeof(Handoff) * NAX * kRing +

@@ -549,7 +549,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
             for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
                 const int c = lane + 32 * s4;
-                ypre[s4] = c < nc ? xr[c0 + c] : 0.0;
+                // L2 read: another SM wrote this half of x in the previous epoch, and a line of it
+                // may still sit in this SM's (non-coherent) L1 from an older epoch
+                ypre[s4] = c < nc ? ld_relaxed_f64(&xr[c0 + c]) : 0.0;
                 tpre[s4] = c < nc ? P.tau[c0 + c] : 1.0;
             }
             // all G partials of sequence k published?  (flush the pending completion before
@@ -579,7 +581,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         for (long long qq = 0; qq < P.G; ++qq) g += ld_relaxed_f64(&P.part[qq * Bmax + c]);
                     } else {
                         g = ld_relaxed_f64(&gacc[c]);
-                        gnext[c] = 0.0;  // the slot's next user accumulates into the other half
                     }
                     const long long jj = c0 + c;
                     const double y = ypre[s4];
@@ -589,6 +590,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     dd = xn - y;
                 }
                 if (c < Bpad) dv[c] = dd;
+                // the slot's next user accumulates into the other half: clear ALL Bmax entries
+                // (that user's block may be wider than this one, e.g. after the ragged last block)
+                if (!P.deterministic && c < Bmax) gnext[c] = 0.0;
                 nz |= dd != 0.0;
             }
             nz = __any_sync(0xffffffffu, nz);

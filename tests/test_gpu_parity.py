@@ -210,6 +210,45 @@ def test_async_reaches_oracle_solution(A, case, schedule):
         S.close()
 
 
+def test_async_long_launch_slot_reuse_ragged(A):
+    """One launch of 300 sweeps of a ragged-n problem: every accumulator slot is reused
+    several times and the ragged last block's slot is next used by full blocks
+    (regression: the accumulator half must be cleared over all B entries)."""
+    P = make_case("dense_ragged")
+    x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
+    S = A.Solver(P)
+    try:
+        S.solve(sweeps=300, reset=True)
+        out = S.stationarity()
+        assert _rel_f(out.objective, F_star) <= 1e-9 and out.mf_norm2 <= 1e-8, (out.objective, F_star, out.mf_norm2)
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("case", ["dense_ragged", "large_block", "nonconvex"])
+def test_reread_path_parity(A, case, monkeypatch):
+    """Panels that are not parked in TMEM are re-read from HBM/L2 by the axpy warps;
+    force that path (ASY_NO_TMEM) and check sequential parity and async convergence."""
+    monkeypatch.setenv("ASY_NO_TMEM", "1")
+    P = make_case(case)
+    S = A.Solver(P)
+    try:
+        S.solve(sweeps=4, max_delay=0, reset=True)
+        x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 4))
+        assert _rel_x(S.x(), x_or) <= REL
+        x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
+        S.solve(sweeps=0, reset=True)
+        for _ in range(60):
+            S.solve(sweeps=100)
+            out = S.stationarity()
+            meas = out.merit_inf if P.c > 0 else out.mf_norm2
+            if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
+                break
+        assert _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5
+    finally:
+        S.close()
+
+
 def test_async_delay_window_respected_tiny(A):
     """configs[0] with all CTAs and an unbounded window diverges like Jacobi;
     the default window (N/8) converges (Theorem 1: gamma vs delta [PAPER.md:301])."""
