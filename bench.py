@@ -141,6 +141,20 @@ def traffic_for(P):
         return None
 
 
+def reduce_over_ranks(ms: float, units: float, world: int, device="cpu"):
+    """Replica timing (replicas only): the job time is the MAX of the
+    ranks' device times, the work is the SUM of their units."""
+    if world <= 1:
+        return ms, units
+    import torch
+    import torch.distributed as dist
+    mx = torch.tensor([ms], dtype=torch.float64, device=device)
+    sm = torch.tensor([units], dtype=torch.float64, device=device)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return mx.item(), sm.item()
+
+
 # ----------------------------------------------------------------------------- oracle arms
 def oracle_rate(P, seconds, x0=None):
     """Sequential Algorithm 1 (d = 0) of the oracle, as it stands, on host cores:
@@ -227,16 +241,7 @@ def run_ours(args, rank, world, local):
     launches = sum(r[1] for r in res)
     kernel_ms = sum(r[2] for r in res)
     sweeps = sum(r[3] for r in res)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([tot_ms, updates], dtype=torch.float64, device=f"cuda:{local}")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        tot_ms_all, updates_all = mx[0].item(), sm[1].item()
-    else:
-        tot_ms_all, updates_all = tot_ms, updates
+    tot_ms_all, updates_all = reduce_over_ranks(tot_ms, updates, world, device=f"cuda:{local}")
 
     # roofline of the fused async kernel: algorithmic bytes / its device time
     hbm_peak, peak_kind = peaks()
