@@ -625,9 +625,16 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     Dev trace;
     if (tr && atoll(tr) > 0) {
         P.trace_n = std::min<int64_t>(atoll(tr), P.T);
-        TRY(dev_alloc(h, trace, sizeof(unsigned long long) * 8 * P.trace_n));
-        CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 8 * P.trace_n, h->stream));
+        TRY(dev_alloc(h, trace, sizeof(unsigned long long) * 12 * P.trace_n));
+        CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 12 * P.trace_n, h->stream));
         P.trace = P_<unsigned long long>(trace);
+    }
+    const char* pf = getenv("ASY_PROF");
+    Dev prof;
+    if (pf) {
+        TRY(dev_alloc(h, prof, sizeof(unsigned long long) * geo.grid * 16 * 8));
+        CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * geo.grid * 16 * 8, h->stream));
+        P.prof = P_<unsigned long long>(prof);
     }
     dense_async_init<<<grid_for(std::max<int64_t>(2 * slots * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
@@ -640,8 +647,18 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
     if (sweeps & 1) std::swap(h->x, h->xalt);  // the updated iterate lives in the other half
+    if (P.prof) {
+        std::vector<unsigned long long> hb((size_t)geo.grid * 16 * 8);
+        CK(cudaMemcpy(hb.data(), prof.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
+        FILE* f = fopen(pf, "wb");
+        if (f) {
+            fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+            fclose(f);
+        }
+        dev_free(prof);
+    }
     if (P.trace) {
-        std::vector<unsigned long long> hb(8 * P.trace_n);
+        std::vector<unsigned long long> hb(12 * P.trace_n);
         CK(cudaMemcpy(hb.data(), trace.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
         const char* fn = getenv("ASY_TRACE_FILE");
         FILE* f = fopen(fn ? fn : "asy_trace.bin", "wb");

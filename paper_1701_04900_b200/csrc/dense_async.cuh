@@ -104,6 +104,7 @@ struct DenseAsyncParams {
     int64_t slots;       // power of two
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
+    unsigned long long* prof;   // optional [grid][warps][8] clock64 segment sums (debug; null = off)
     unsigned long long* trace;  // optional [trace_n][8] globaltimer stamps (debug; null = off)
     int64_t trace_n;
 };
@@ -116,11 +117,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define ASY_TRACE(P_, t_, slot_)                                                   \
     do {                                                                           \
         if ((P_).trace && (t_) >= 0 && (t_) < (P_).trace_n && lane == 0)           \
-            (P_).trace[(t_) * 8 + (slot_)] = gtimer();                             \
+            (P_).trace[(t_) * 12 + (slot_)] = gtimer();                             \
     } while (0)
 
 struct StageMeta {
     long long t, k, b, p;
+};
+
+// clock64 segment profiler (debug): seg[i] += cycles since the previous mark
+struct SegProf {
+    unsigned long long seg[8];
+    long long last;
+    __device__ void start() {
+        for (int i = 0; i < 8; ++i) seg[i] = 0;
+        last = clock64();
+    }
+    __device__ void mark(int i) {
+        const long long t = clock64();
+        seg[i] += (unsigned long long)(t - last);
+        last = t;
+    }
+    __device__ void flush(unsigned long long* out, int lane) {
+        if (out && lane == 0)
+            for (int i = 0; i < 8; ++i) out[i] = seg[i];
+    }
 };
 
 struct Handoff {
@@ -237,6 +257,9 @@ __device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_volatile_cta_u32(unsigned* p, unsigned v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
@@ -389,6 +412,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * q) << 16);
         double* wsm = wbuf + q * R;
         unsigned tm_used = 0u;  // panels parked by this pair so far (slot = tm_used % kTmemSlots)
+        SegProf sp;
+        sp.start();
         for (long long j = 0;; ++j) {
             const long long it = j * kPairs + q;  // pair q owns stage q
             const int st = (int)(it % NS);
@@ -400,6 +425,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             uint64_t* rf = &rfull[(q * kAxpyPerPair + h) * kRing + rs];
             uint64_t* re = &rempty[(q * kAxpyPerPair + h) * kRing + rs];
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
+            sp.mark(0);
             const StageMeta md = meta[st];
             if (md.t < 0) {
                 if (lane == 0) mbar_arrive(&empty[st]);
@@ -426,6 +452,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 wsm[i] = (r0 + i) < P.m ? loss_prime(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
             __syncwarp();
+            sp.mark(1);
             // pass 1: A_{b,p}^T w from shared memory
             for (int g0 = 0; g0 < Bmax; g0 += 16) {
                 const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;  // valid smem columns in group
@@ -448,6 +475,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             ASY_TRACE(P, md.t, 3);
+            sp.mark(2);
             // park in the axpy warp's TMEM slot if it is free; otherwise the axpy re-reads A
             // (bounded wait: holding the stage indefinitely could hold back a block whose
             // panel is queued behind it, so after kParkWaitNs the panel is left in HBM/L2)
@@ -467,6 +495,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 parked = __shfl_sync(0xffffffffu, ok, 0);
             }
             ASY_TRACE(P, md.t, 4);
+            sp.mark(3);
             const int tslot_idx = (int)(tm_used % kTmemSlots);
             if (parked) {
                 tc_fence_after();
@@ -490,6 +519,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 tc_fence_before();
             }
             __syncwarp();
+            sp.mark(4);
             // publish (the partials' red.adds drained during the parking pass)
             if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);
             // hand-off note (after publishing: waiting here can never hold back a block)
@@ -500,7 +530,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 ho->parked = parked ? 1 + tslot_idx : 0;
                 mbar_arrive(rf);
             }
+            sp.mark(5);
         }
+        sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * 16 + warp) * 8 : nullptr, lane);
     } else {
         // ------------------------------------------------------------------ axpy warps
         const int q = warp, h = 0;
@@ -520,6 +552,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             pend_slot = -1;
         };
+        SegProf sp;
+        sp.start();
         for (long long e = 0;; ++e) {
             const int rs = (int)(e % kRing);
             // the previous panel's completion is issued now unless the next one is already here;
@@ -531,6 +565,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const Handoff hd = myring[rs];
             __syncwarp();
             if (lane == 0) mbar_arrive(&myempty[rs]);
+            sp.mark(0);
             const StageMeta md = hd.md;
             if (md.t < 0) break;
             const long long k = md.k, b = md.b, p = md.p;
@@ -568,6 +603,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             __syncwarp();
             ASY_TRACE(P, md.t, 6);
+            sp.mark(1);
             // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block
             bool nz = false;
 #pragma unroll
@@ -597,6 +633,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             nz = __any_sync(0xffffffffu, nz);
             __syncwarp();
+            sp.mark(2);
+            // the previous panel's completion: its red.adds were issued a whole panel ago, so this
+            // fence rarely waits (issued after this panel's red.adds it always would)
+            complete();
+            sp.mark(3);
+            ASY_TRACE(P, md.t, 8);
             const long long r0 = p * R;
             if (hd.parked) tc_fence_after();
             if (nz) {
@@ -607,20 +649,35 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     if (hd.parked) {
                         const uint32_t trow = tquarter + (uint32_t)((hd.parked - 1) * kSlotCols + qq * cols_per_row);
 #pragma unroll 1
-                        for (int c8 = 0; c8 < Bpad; c8 += 8) {
-                            uint32_t uu[16];
-                            tmem_ld8(trow + 2 * c8, uu);
-                            const double2* d2 = reinterpret_cast<const double2*>(dv + c8);  // LDS.128 broadcast
-                            const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
+                        for (int c32 = 0; c32 < Bpad; c32 += 32) {
+                            // up to 32 doubles of the row in one batch of TMEM loads, one wait
+                            const int n8 = (Bpad - c32) >= 32 ? 4 : (Bpad - c32) / 8;
+                            uint32_t uu[64];
+#ifdef ASY_DIAG_NO_TMEMLD
+#pragma unroll
+                            for (int i = 0; i < 64; ++i) uu[i] = trow + i;
+#else
+#pragma unroll
+                            for (int s8 = 0; s8 < 4; ++s8)
+                                if (s8 < n8) tmem_ld8(trow + 2 * (c32 + 8 * s8), uu + 16 * s8);
                             tmem_wait_ld();
-                            acc4[0] = fma(u2d(uu[0], uu[1]), da.x, acc4[0]);
-                            acc4[1] = fma(u2d(uu[2], uu[3]), da.y, acc4[1]);
-                            acc4[2] = fma(u2d(uu[4], uu[5]), db.x, acc4[2]);
-                            acc4[3] = fma(u2d(uu[6], uu[7]), db.y, acc4[3]);
-                            acc4[0] = fma(u2d(uu[8], uu[9]), dc.x, acc4[0]);
-                            acc4[1] = fma(u2d(uu[10], uu[11]), dc.y, acc4[1]);
-                            acc4[2] = fma(u2d(uu[12], uu[13]), dd2.x, acc4[2]);
-                            acc4[3] = fma(u2d(uu[14], uu[15]), dd2.y, acc4[3]);
+#endif
+#pragma unroll
+                            for (int s8 = 0; s8 < 4; ++s8) {
+                                if (s8 < n8) {
+                                    const double2* d2 = reinterpret_cast<const double2*>(dv + c32 + 8 * s8);
+                                    const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
+                                    const uint32_t* w = uu + 16 * s8;
+                                    acc4[0] = fma(u2d(w[0], w[1]), da.x, acc4[0]);
+                                    acc4[1] = fma(u2d(w[2], w[3]), da.y, acc4[1]);
+                                    acc4[2] = fma(u2d(w[4], w[5]), db.x, acc4[2]);
+                                    acc4[3] = fma(u2d(w[6], w[7]), db.y, acc4[3]);
+                                    acc4[0] = fma(u2d(w[8], w[9]), dc.x, acc4[0]);
+                                    acc4[1] = fma(u2d(w[10], w[11]), dc.y, acc4[1]);
+                                    acc4[2] = fma(u2d(w[12], w[13]), dd2.x, acc4[2]);
+                                    acc4[3] = fma(u2d(w[14], w[15]), dd2.y, acc4[3]);
+                                }
+                            }
                         }
                     } else if (row < P.m) {
                         // re-read the panel row from global memory (L2, usually)
@@ -635,22 +692,31 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         }
                     }
                     const double dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+#ifdef ASY_DIAG_NO_RED
+                    if (row < P.m && dsum == 12345.0) P.r[row] = dsum;
+#else
                     if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
+#endif
                 }
             }
+            ASY_TRACE(P, md.t, 9);
+            sp.mark(4);
             if (hd.parked) {
+                // TMEM slot free.  The loads completed (wait::ld), so a plain store is enough; a
+                // release store would also wait for this panel's red.adds to reach L2.
                 tc_fence_before();
                 __syncwarp();
                 ++tm_fin;
-                if (lane == 0) st_release_cta_u32(&tm_done[ax], tm_fin);  // TMEM slot free
+                if (lane == 0) st_volatile_cta_u32(&tm_done[ax], tm_fin);
             }
             __syncwarp();
             ASY_TRACE(P, md.t, 7);
-            complete();  // the one before this panel (if not flushed above)
             pend_slot = slot;
             pend_b = b;
+            sp.mark(5);
         }
         complete();
+        sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * 16 + warp) * 8 : nullptr, lane);
     }
     tc_fence_before();
     __syncthreads();
