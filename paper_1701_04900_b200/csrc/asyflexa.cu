@@ -543,30 +543,46 @@ struct DenseGeom {
     int64_t R, G, delay;
     int Bpad, grid, use_tmem;
     size_t smem;
+    const void* kernel;
 };
+
+// compiled (BT, RPL) instantiations of dense_async_kernel: BT = block width padded to
+// {8,16,32,64,128}, RPL = panel rows per lane; default R*BT = 4096 doubles (32 KB panels)
+using DenseKernelFn = void (*)(const CUtensorMap, const DenseAsyncParams);
+static DenseKernelFn dense_kernel_for(int BT, int RPL) {
+#define ASY_DK(bt, rpl) if (BT == bt && RPL == rpl) return dense_async_kernel<bt, rpl>;
+    ASY_DK(8, 8) ASY_DK(8, 4) ASY_DK(16, 8) ASY_DK(16, 4) ASY_DK(32, 4) ASY_DK(32, 2)
+    ASY_DK(64, 2) ASY_DK(64, 1) ASY_DK(128, 1)
+#undef ASY_DK
+    return nullptr;
+}
 
 static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t delay, DenseGeom* g) {
     const int64_t B = h->B;
-    const int64_t Bpad = (B + 7) / 8 * 8;
-    int64_t R = sp->panel_rows;
-    if (R <= 0) R = 4096 / B;                       // ~32 KB panels
-    R = (R + 31) / 32 * 32;
-    R = std::max<int64_t>(32, std::min<int64_t>(R, 256));
-    const int64_t mr = (h->m + 31) / 32 * 32;
-    if (R > mr) R = mr;
+    int BT = 8;
+    while (BT < B) BT *= 2;
+    const int rpl_default = std::max(1, std::min(8, 4096 / BT / 32));
+    int RPL = rpl_default;
+    if (sp->panel_rows > 0) {
+        const int want = sp->panel_rows / 32;
+        RPL = dense_kernel_for(BT, want) ? want : rpl_default;
+    }
+    const int64_t R = 32 * RPL;
     const int64_t G = (h->m + R - 1) / R;
-    int use_tmem = (R / 32) * 2 * Bpad <= kSlotCols;
+    DenseKernelFn fn = dense_kernel_for(BT, RPL);
+    if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no dense kernel for block width %d", BT);
+    int use_tmem = RPL * 2 * BT <= kSlotCols;
     if (getenv("ASY_NO_TMEM")) use_tmem = 0;  // debug/test: force the re-read path
     constexpr int NAX = kPairs * kAxpyPerPair;
-    const size_t smem = sizeof(double) * (kPairs * (R * B + 2 * R) + NAX * Bpad + kPairs * R) +
+    const size_t smem = sizeof(double) * (kPairs * (R * BT + 2 * R) + NAX * BT + kPairs * R) +
                         sizeof(StageMeta) * (kPairs + kQueue) + sizeof(Handoff) * NAX * kRing +
                         sizeof(uint64_t) * (2 * kPairs + 2 * kQueue + 2 * NAX * kRing) + sizeof(unsigned) * (NAX + 1) +
                         64;
     if (smem > 227 * 1024)
         return h->fail(ASY_ERR_INVALID, "panel_rows*block_size too large for shared memory (%zu B)", smem);
-    CK(cudaFuncSetAttribute(dense_async_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dense_async_kernel, kDenseThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kDenseThreads, smem));
     if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense async kernel does not fit on an SM");
     int grid = h->sms;  // one CTA per SM: it owns the SM's whole TMEM (512 columns)
     // enough workers to keep ~2x the delay window of panels in flight, never more
@@ -576,7 +592,8 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     // blocks in flight are capped so that a block's panels never fill an axpy warp's hand-off ring
     const int64_t cap = std::max<int64_t>(0, (int64_t)kRing * NAX * grid / (4 * G) - 1);
     g->delay = std::min<int64_t>(delay, cap);
-    g->R = R; g->G = G; g->Bpad = (int)Bpad; g->grid = grid; g->smem = smem; g->use_tmem = use_tmem;
+    g->R = R; g->G = G; g->Bpad = BT; g->grid = grid; g->smem = smem; g->use_tmem = use_tmem;
+    g->kernel = (const void*)fn;
     return ASY_OK;
 }
 
@@ -591,7 +608,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CUtensorMap tmap;
     cuuint64_t dims[2] = {(cuuint64_t)h->m, (cuuint64_t)h->n};
     cuuint64_t strides[1] = {(cuuint64_t)(h->lda * sizeof(double))};
-    cuuint32_t box[2] = {(cuuint32_t)R, (cuuint32_t)B};
+    cuuint32_t box[2] = {(cuuint32_t)R, (cuuint32_t)geo.Bpad};  // BT columns (extra ones are OOB zeros / ignored)
     cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->A.p, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -640,8 +657,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CKL();
     void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));
-    CK(cudaLaunchCooperativeKernel((void*)dense_async_kernel, dim3(geo.grid), dim3(kDenseThreads), args, geo.smem,
-                                   h->stream));
+    CK(cudaLaunchCooperativeKernel(geo.kernel, dim3(geo.grid), dim3(kDenseThreads), args, geo.smem, h->stream));
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();

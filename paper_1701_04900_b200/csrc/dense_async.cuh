@@ -265,15 +265,37 @@ __device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
+// Butterfly reduce-scatter over 8 columns: lanes with l & 7 == c return column c's total.
+__device__ __forceinline__ double transpose_reduce8(double (&v)[8], int lane) {
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o];
+            const double keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    const double t = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 8);
+    return t + __shfl_xor_sync(0xffffffffu, t, 16);
+}
+
+// BT = block width padded to a multiple of 8 (panel columns, TMEM row layout);
+// RPL = panel rows per lane (R = 32*RPL).  Both compile-time so that the inner
+// loops are fully unrolled with immediate shared-memory offsets.
+template <int BT, int RPL>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     constexpr int NS = kPairs;               // one stage per pair
     constexpr int NAX = kPairs * kAxpyPerPair;
-    const int R = (int)P.R;
-    const int Bmax = P.Bmax, Bpad = P.Bpad;
-    const size_t PANEL = (size_t)R * Bmax;   // doubles of A per stage
-    const size_t STAGE = PANEL + 2 * R;      // + the R residual rows + the R rows of b / y
+    constexpr int R = 32 * RPL;
+    constexpr int Bpad = BT;
+    constexpr int GW = BT < 16 ? BT : 16;    // column group of the dot pass
+    const int Bmax = P.Bmax;
+    constexpr size_t PANEL = (size_t)R * BT;  // doubles of A per stage (TMA box R x BT)
+    constexpr size_t STAGE = PANEL + 2 * R;   // + the R residual rows + the R rows of b / y
     double* stages = reinterpret_cast<double*>(smem_raw);                       // NS * STAGE
     double* dxs = stages + NS * STAGE;                                          // NAX * Bpad
     double* wbuf = dxs + NAX * Bpad;                                            // kPairs * R
@@ -305,8 +327,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_s;
-    const int rows_per_lane = R / 32;
-    const int cols_per_row = 2 * Bpad;  // b32 TMEM columns per panel row
+    constexpr int rows_per_lane = RPL;
+    constexpr int cols_per_row = 2 * Bpad;  // b32 TMEM columns per panel row
 
     if (warp == kProducerWarp) {
         // ------------------------------------------------------------------ producer
@@ -410,7 +432,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         // ------------------------------------------------------------------ dot warps
         const int q = warp - kPairs;
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * q) << 16);
-        double* wsm = wbuf + q * R;
         unsigned tm_used = 0u;  // panels parked by this pair so far (slot = tm_used % kTmemSlots)
         SegProf sp;
         sp.start();
@@ -445,75 +466,87 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const double* pan = stages + st * STAGE;
             const double* rsm = pan + PANEL;
             ASY_TRACE(P, md.t, 2);
-            // w = phi'(r) on the panel rows (residual and b / y rows arrived with the panel)
+            // w = phi'(r) on this lane's panel rows (residual and b / y rows arrived with the panel)
             const long long r0 = p * R;
-            for (int qq = 0; qq < rows_per_lane; ++qq) {
+            double w[RPL];
+#pragma unroll
+            for (int qq = 0; qq < RPL; ++qq) {
                 const int i = lane + 32 * qq;
-                wsm[i] = (r0 + i) < P.m ? loss_prime(P.S, rsm[i], rsm[R + i]) : 0.0;
+                w[qq] = (r0 + i) < P.m ? loss_prime(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
-            __syncwarp();
             sp.mark(1);
-            // pass 1: A_{b,p}^T w from shared memory
-            for (int g0 = 0; g0 < Bmax; g0 += 16) {
-                const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;  // valid smem columns in group
-                double acc[16];
+            // a free TMEM slot now?  then dot and park in ONE pass over shared memory
+            int parked = 0;
+            if (P.use_tmem) {
+                unsigned ok = 0;
+                if (lane == 0) ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                parked = __shfl_sync(0xffffffffu, ok, 0);
+                if (parked) tc_fence_after();
+            }
+            const int tslot_idx = (int)(tm_used % kTmemSlots);
+            const uint32_t tslot = tlane + (uint32_t)(tslot_idx * kSlotCols);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) acc[c] = 0.0;
-#pragma unroll 2
-                for (int qq = 0; qq < rows_per_lane; ++qq) {
-                    const int i = lane + 32 * qq;
-                    const double w = wsm[i];
-                    const double* a = pan + (size_t)g0 * R + i;
+            for (int g0 = 0; g0 < BT; g0 += GW) {
+                double acc[GW];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c)
-                        if (c < ncg) acc[c] = fma(a[(size_t)c * R], w, acc[c]);
+                for (int c = 0; c < GW; ++c) acc[c] = 0.0;
+#pragma unroll
+                for (int qq = 0; qq < RPL; ++qq) {
+                    const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
+                    double v[GW];
+#pragma unroll
+                    for (int c = 0; c < GW; ++c) v[c] = a[c * R];
+#pragma unroll
+                    for (int c = 0; c < GW; ++c) acc[c] = fma(v[c], w[qq], acc[c]);
+                    if (parked) {
+                        const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
+#pragma unroll
+                        for (int s8 = 0; s8 < GW / 8; ++s8) tmem_st8(trow + 16 * s8, v + 8 * s8);
+                    }
                 }
-                const double colsum = transpose_reduce16(acc, lane);
-                if (lane < ncg && g0 + lane < nc) {
+                double colsum;
+                if constexpr (GW == 16) colsum = transpose_reduce16(acc, lane);
+                else colsum = transpose_reduce8(acc, lane);
+                if (lane < GW && g0 + lane < nc) {
                     if (P.deterministic) P.part[p * Bmax + g0 + lane] = colsum;
                     else atomicAdd(&gacc[g0 + lane], colsum);
                 }
             }
             ASY_TRACE(P, md.t, 3);
             sp.mark(2);
-            // park in the axpy warp's TMEM slot if it is free; otherwise the axpy re-reads A
-            // (bounded wait: holding the stage indefinitely could hold back a block whose
-            // panel is queued behind it, so after kParkWaitNs the panel is left in HBM/L2)
-            int parked = 0;
-            if (P.use_tmem) {
+            if (!parked && P.use_tmem) {
+                // no slot was free: wait a bounded time for one, then park in a second pass;
+                // holding the stage indefinitely could hold back a block whose panel is queued
+                // behind it, so after kParkWaitNs the panel is left in HBM/L2 (re-read later)
                 unsigned ok = 0;
                 if (lane == 0) {
-                    ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
-                    if (!ok) {
-                        const unsigned long long t0 = gtimer();
-                        do {
-                            __nanosleep(64);
-                            ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
-                        } while (!ok && gtimer() - t0 < kParkWaitNs);
-                    }
+                    const unsigned long long t0 = gtimer();
+                    do {
+                        __nanosleep(64);
+                        ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                    } while (!ok && gtimer() - t0 < kParkWaitNs);
                 }
                 parked = __shfl_sync(0xffffffffu, ok, 0);
-            }
-            ASY_TRACE(P, md.t, 4);
-            sp.mark(3);
-            const int tslot_idx = (int)(tm_used % kTmemSlots);
-            if (parked) {
-                tc_fence_after();
-                const uint32_t tslot = tlane + (uint32_t)(tslot_idx * kSlotCols);
-                for (int g0 = 0; g0 < Bpad; g0 += 16) {
-                    const int ncg = (Bmax - g0) < 16 ? (Bmax - g0) : 16;
-                    const int npg = (Bpad - g0) < 16 ? (Bpad - g0) : 16;
-#pragma unroll 1
-                    for (int qq = 0; qq < rows_per_lane; ++qq) {
-                        const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
-                        double v[16];
+                ASY_TRACE(P, md.t, 4);
+                sp.mark(3);
+                if (parked) {
+                    tc_fence_after();
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) v[c] = c < ncg ? a[(size_t)c * R] : 0.0;
-                        const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
-                        tmem_st8(trow, v);
-                        if (npg > 8) tmem_st8(trow + 16, v + 8);
+                    for (int g0 = 0; g0 < BT; g0 += GW) {
+#pragma unroll
+                        for (int qq = 0; qq < RPL; ++qq) {
+                            const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
+                            double v[GW];
+#pragma unroll
+                            for (int c = 0; c < GW; ++c) v[c] = a[c * R];
+                            const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
+#pragma unroll
+                            for (int s8 = 0; s8 < GW / 8; ++s8) tmem_st8(trow + 16 * s8, v + 8 * s8);
+                        }
                     }
                 }
+            }
+            if (parked) {
                 ++tm_used;
                 tmem_wait_st();
                 tc_fence_before();
@@ -642,41 +675,24 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long r0 = p * R;
             if (hd.parked) tc_fence_after();
             if (nz) {
-#pragma unroll 1
-                for (int qq = 0; qq < rows_per_lane; ++qq) {
+#pragma unroll
+                for (int qq = 0; qq < RPL; ++qq) {
                     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
                     const long long row = r0 + lane + 32 * qq;
                     if (hd.parked) {
                         const uint32_t trow = tquarter + (uint32_t)((hd.parked - 1) * kSlotCols + qq * cols_per_row);
-#pragma unroll 1
-                        for (int c32 = 0; c32 < Bpad; c32 += 32) {
-                            // up to 32 doubles of the row in one batch of TMEM loads, one wait
-                            const int n8 = (Bpad - c32) >= 32 ? 4 : (Bpad - c32) / 8;
-                            uint32_t uu[64];
-#ifdef ASY_DIAG_NO_TMEMLD
 #pragma unroll
-                            for (int i = 0; i < 64; ++i) uu[i] = trow + i;
-#else
+                        for (int c32 = 0; c32 < BT; c32 += 32) {
+                            constexpr int n8max = BT < 32 ? BT / 8 : 4;
+                            uint32_t uu[16 * n8max];
 #pragma unroll
-                            for (int s8 = 0; s8 < 4; ++s8)
-                                if (s8 < n8) tmem_ld8(trow + 2 * (c32 + 8 * s8), uu + 16 * s8);
+                            for (int s8 = 0; s8 < n8max; ++s8) tmem_ld8(trow + 2 * (c32 + 8 * s8), uu + 16 * s8);
                             tmem_wait_ld();
-#endif
 #pragma unroll
-                            for (int s8 = 0; s8 < 4; ++s8) {
-                                if (s8 < n8) {
-                                    const double2* d2 = reinterpret_cast<const double2*>(dv + c32 + 8 * s8);
-                                    const double2 da = d2[0], db = d2[1], dc = d2[2], dd2 = d2[3];
-                                    const uint32_t* w = uu + 16 * s8;
-                                    acc4[0] = fma(u2d(w[0], w[1]), da.x, acc4[0]);
-                                    acc4[1] = fma(u2d(w[2], w[3]), da.y, acc4[1]);
-                                    acc4[2] = fma(u2d(w[4], w[5]), db.x, acc4[2]);
-                                    acc4[3] = fma(u2d(w[6], w[7]), db.y, acc4[3]);
-                                    acc4[0] = fma(u2d(w[8], w[9]), dc.x, acc4[0]);
-                                    acc4[1] = fma(u2d(w[10], w[11]), dc.y, acc4[1]);
-                                    acc4[2] = fma(u2d(w[12], w[13]), dd2.x, acc4[2]);
-                                    acc4[3] = fma(u2d(w[14], w[15]), dd2.y, acc4[3]);
-                                }
+                            for (int i = 0; i < 8 * n8max; i += 2) {
+                                const double2 d2 = *reinterpret_cast<const double2*>(dv + c32 + i);
+                                acc4[i & 3] = fma(u2d(uu[2 * i], uu[2 * i + 1]), d2.x, acc4[i & 3]);
+                                acc4[(i + 1) & 3] = fma(u2d(uu[2 * i + 2], uu[2 * i + 3]), d2.y, acc4[(i + 1) & 3]);
                             }
                         }
                     } else if (row < P.m) {
