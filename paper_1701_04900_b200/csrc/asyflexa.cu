@@ -549,10 +549,10 @@ struct DenseGeom {
 // compiled (BT, RPL) instantiations of dense_async_kernel: BT = block width padded to
 // {8,16,32,64,128}, RPL = panel rows per lane; default R*BT = 4096 doubles (32 KB panels)
 using DenseKernelFn = void (*)(const CUtensorMap, const DenseAsyncParams);
-static DenseKernelFn dense_kernel_for(int BT, int RPL) {
-#define ASY_DK(bt, rpl) if (BT == bt && RPL == rpl) return dense_async_kernel<bt, rpl>;
-    ASY_DK(8, 8) ASY_DK(8, 4) ASY_DK(16, 8) ASY_DK(16, 4) ASY_DK(32, 4) ASY_DK(32, 2)
-    ASY_DK(64, 2) ASY_DK(64, 1) ASY_DK(128, 1)
+static DenseKernelFn dense_kernel_for(int BT, int RPL, int NS) {
+#define ASY_DK(bt, rpl, ns) if (BT == bt && RPL == rpl && NS == ns) return dense_async_kernel<bt, rpl, ns>;
+    ASY_DK(8, 8, 4) ASY_DK(8, 4, 8) ASY_DK(16, 8, 4) ASY_DK(16, 4, 8) ASY_DK(32, 4, 4) ASY_DK(32, 3, 8)
+    ASY_DK(32, 2, 8) ASY_DK(64, 2, 4) ASY_DK(64, 1, 8) ASY_DK(128, 1, 4)
 #undef ASY_DK
     return nullptr;
 }
@@ -561,22 +561,27 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int64_t B = h->B;
     int BT = 8;
     while (BT < B) BT *= 2;
-    const int rpl_default = std::max(1, std::min(8, 4096 / BT / 32));
-    int RPL = rpl_default;
+    // (measured on configs 1-3: one 32 KB stage per pair beats two smaller ones -- the
+    // per-panel fixed costs dominate, not the load latency)
+    int RPL = BT == 8 ? 8 : BT == 16 ? 8 : BT == 32 ? 4 : BT == 64 ? 2 : 1;
+    int NS = kPairs;
+    if (getenv("ASY_DENSE_RPL")) RPL = atoi(getenv("ASY_DENSE_RPL"));
+    if (getenv("ASY_DENSE_NS")) NS = atoi(getenv("ASY_DENSE_NS"));
     if (sp->panel_rows > 0) {
         const int want = sp->panel_rows / 32;
-        RPL = dense_kernel_for(BT, want) ? want : rpl_default;
+        if (dense_kernel_for(BT, want, NS)) RPL = want;
+        else if (dense_kernel_for(BT, want, kPairs)) { RPL = want; NS = kPairs; }
     }
     const int64_t R = 32 * RPL;
     const int64_t G = (h->m + R - 1) / R;
-    DenseKernelFn fn = dense_kernel_for(BT, RPL);
-    if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no dense kernel for block width %d", BT);
+    DenseKernelFn fn = dense_kernel_for(BT, RPL, NS);
+    if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no dense kernel for BT=%d RPL=%d NS=%d", BT, RPL, NS);
     int use_tmem = RPL * 2 * BT <= kSlotCols;
     if (getenv("ASY_NO_TMEM")) use_tmem = 0;  // debug/test: force the re-read path
     constexpr int NAX = kPairs * kAxpyPerPair;
-    const size_t smem = sizeof(double) * (kPairs * (R * BT + 2 * R) + NAX * BT + kPairs * R) +
-                        sizeof(StageMeta) * (kPairs + kQueue) + sizeof(Handoff) * NAX * kRing +
-                        sizeof(uint64_t) * (2 * kPairs + 2 * kQueue + 2 * NAX * kRing) + sizeof(unsigned) * (NAX + 1) +
+    const size_t smem = sizeof(double) * (NS * (R * BT + 2 * R) + NAX * BT) +
+                        sizeof(StageMeta) * (NS + kQueue) + sizeof(Handoff) * NAX * kRing +
+                        sizeof(uint64_t) * (2 * NS + 2 * kQueue + 2 * NAX * kRing) + sizeof(unsigned) * (NAX + 1) +
                         64;
     if (smem > 227 * 1024)
         return h->fail(ASY_ERR_INVALID, "panel_rows*block_size too large for shared memory (%zu B)", smem);

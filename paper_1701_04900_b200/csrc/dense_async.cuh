@@ -65,7 +65,7 @@ constexpr int kProducerWarp = 8;
 constexpr int kSchedWarp = 9;
 constexpr int kDenseThreads = 32 * 10;
 constexpr int kQueue = 4;            // scheduler -> producer queue depth
-constexpr int kRing = 64;            // hand-off notes per axpy warp
+constexpr int kRing = 32;            // hand-off notes per axpy warp
 constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
 constexpr int kClaim = 4;            // subtasks claimed per atomic
 constexpr int kSlotCols = 256;       // TMEM columns per parked panel
@@ -281,14 +281,16 @@ __device__ __forceinline__ double transpose_reduce8(double (&v)[8], int lane) {
     return t + __shfl_xor_sync(0xffffffffu, t, 16);
 }
 
-// BT = block width padded to a multiple of 8 (panel columns, TMEM row layout);
-// RPL = panel rows per lane (R = 32*RPL).  Both compile-time so that the inner
-// loops are fully unrolled with immediate shared-memory offsets.
-template <int BT, int RPL>
+// BT = block width padded to a power of two >= 8 (panel columns, TMEM row layout);
+// RPL = panel rows per lane (R = 32*RPL); NS = smem stages (kPairs or 2*kPairs:
+// a second stage per pair overlaps the next panel's load with this one's dot).
+// All compile-time so that the inner loops are fully unrolled with immediate
+// shared-memory offsets.
+template <int BT, int RPL, int NS>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    constexpr int NS = kPairs;               // one stage per pair
+    static_assert(NS % kPairs == 0, "pair q owns stages q (mod kPairs)");
     constexpr int NAX = kPairs * kAxpyPerPair;
     constexpr int R = 32 * RPL;
     constexpr int Bpad = BT;
@@ -298,8 +300,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     constexpr size_t STAGE = PANEL + 2 * R;   // + the R residual rows + the R rows of b / y
     double* stages = reinterpret_cast<double*>(smem_raw);                       // NS * STAGE
     double* dxs = stages + NS * STAGE;                                          // NAX * Bpad
-    double* wbuf = dxs + NAX * Bpad;                                            // kPairs * R
-    StageMeta* meta = reinterpret_cast<StageMeta*>(wbuf + kPairs * R);         // NS
+    StageMeta* meta = reinterpret_cast<StageMeta*>(dxs + NAX * Bpad);          // NS
     StageMeta* queue = meta + NS;                                               // kQueue
     Handoff* ring = reinterpret_cast<Handoff*>(queue + kQueue);                 // NAX * kRing
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + NAX * kRing);           // NS
