@@ -189,6 +189,12 @@ ASY_API void asy_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uin
 ASY_API int asy_schedule_block(int32_t schedule, uint64_t seed, int64_t nblocks, int64_t k,
                                int64_t* out);
 
+/* Global index of the previous update of the block that sequence k updates
+ * (every epoch visits each block once, so it lies in epoch k/N - 1), or -1 in
+ * epoch 0.  The dense async kernel uses it for Assumption D4 [PAPER.md:233]:
+ * a block is not read again before its previous update is applied. */
+ASY_API int asy_schedule_prev(int32_t schedule, uint64_t seed, int64_t nblocks, int64_t k, int64_t* out);
+
 /* Device evaluation of the same schedule for k = k0..k0+count-1 (written to the
  * HOST array out); lets tests check host == device bit for bit. */
 ASY_API int asy_schedule_device(asy_handle* h, int32_t schedule, uint64_t seed, int64_t nblocks,

@@ -76,9 +76,10 @@ _lib.asy_version.restype = C.c_char_p
 _lib.asy_philox4x32_10.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
 _lib.asy_philox4x32_10.restype = None
 _lib.asy_schedule_block.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]
+_lib.asy_schedule_prev.argtypes = [C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]
 _lib.asy_schedule_device.argtypes = [_H, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, _vp]
 for _f in ("asy_create", "asy_destroy", "asy_set_problem", "asy_solve", "asy_stationarity",
-           "asy_get_x", "asy_objective", "asy_schedule_block", "asy_schedule_device"):
+           "asy_get_x", "asy_objective", "asy_schedule_block", "asy_schedule_prev", "asy_schedule_device"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -152,6 +153,14 @@ def asy_schedule_block(schedule: int, seed: int, nblocks: int, k: int) -> int:
     code = _lib.asy_schedule_block(schedule, seed, nblocks, k, C.byref(out))
     if code != ASY_OK:
         raise AsyError(code, "asy_schedule_block: invalid arguments")
+    return out.value
+
+
+def asy_schedule_prev(schedule: int, seed: int, nblocks: int, k: int) -> int:
+    out = C.c_int64()
+    code = _lib.asy_schedule_prev(schedule, seed, nblocks, k, C.byref(out))
+    if code != ASY_OK:
+        raise AsyError(code, "asy_schedule_prev: invalid arguments")
     return out.value
 
 

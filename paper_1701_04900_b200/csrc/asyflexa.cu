@@ -21,6 +21,7 @@
 #include "../../include/asyflexa.h"
 #include "common.cuh"
 #include "dense_async.cuh"
+#include "dense_slab.cuh"
 #include "sparse_async.cuh"
 #include "sync_kernels.cuh"
 
@@ -244,6 +245,13 @@ ASY_API int asy_schedule_block(int32_t schedule, uint64_t seed, int64_t nblocks,
     if (!out || nblocks < 1 || k < 0 || (schedule != ASY_SCHED_CYCLIC && schedule != ASY_SCHED_RANDOM))
         return ASY_ERR_INVALID;
     *out = schedule_block(schedule, seed, nblocks, k);
+    return ASY_OK;
+}
+
+ASY_API int asy_schedule_prev(int32_t schedule, uint64_t seed, int64_t nblocks, int64_t k, int64_t* out) {
+    if (!out || nblocks < 1 || k < 0 || (schedule != ASY_SCHED_CYCLIC && schedule != ASY_SCHED_RANDOM))
+        return ASY_ERR_INVALID;
+    *out = schedule_prev(schedule, seed, nblocks, k, schedule_block(schedule, seed, nblocks, k));
     return ASY_OK;
 }
 
@@ -692,6 +700,167 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     return ASY_OK;
 }
 
+// ---- row-slab dense async kernel (dense_slab.cuh)
+using SlabKernelFn = void (*)(const CUtensorMap, const SlabParams);
+static SlabKernelFn slab_kernel_for(int cpw, int loss) {
+    if (loss == LOSS_LS) {
+        if (cpw == 8) return dense_slab_kernel<8, LOSS_LS>;
+        if (cpw == 16) return dense_slab_kernel<16, LOSS_LS>;
+        if (cpw == 32) return dense_slab_kernel<32, LOSS_LS>;
+    } else {
+        if (cpw == 8) return dense_slab_kernel<8, LOSS_LOGISTIC>;
+        if (cpw == 16) return dense_slab_kernel<16, LOSS_LOGISTIC>;
+        if (cpw == 32) return dense_slab_kernel<32, LOSS_LOGISTIC>;
+    }
+    return nullptr;
+}
+
+static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay, float* ms) {
+    const int64_t m = h->m, B = h->B;
+    const int cpw = B <= 32 ? 8 : B <= 64 ? 16 : 32;
+    const int BMAX = kSlabDot * cpw;
+    if (B > BMAX) return h->fail(ASY_ERR_UNSUPPORTED, "block size %lld > %d", (long long)B, BMAX);
+    // slabs: one CTA per SM, at least 16 rows each, every CTA owns >= 1 row
+    int64_t grid0 = h->sms;
+    if (sp->workers > 0) grid0 = std::min<int64_t>(grid0, sp->workers);
+    grid0 = std::max<int64_t>(1, std::min<int64_t>(grid0, (m + 15) / 16));
+    int64_t Rs = (m + grid0 - 1) / grid0;
+    Rs += Rs & 1;  // even: 16-byte aligned TMA row starts
+    const int grid = (int)((m + Rs - 1) / Rs);
+    // chunks of Rc rows (TMA box Rc x B, Rc even, <= 256): fewest rows loaded past the slab,
+    // then fewest chunks, with stages of at most ~24 KB (ASY_SLAB_CHUNK_KB)
+    int nch = 0, Rc = 0;
+    {
+        const char* ckb = getenv("ASY_SLAB_CHUNK_KB");
+        const int64_t chunk_bytes = 1024 * (ckb ? std::max(1, atoi(ckb)) : 24);
+        const int64_t max_rows = std::max<int64_t>(2, std::min<int64_t>(256, (chunk_bytes / (8 * BMAX)) & ~1ll));
+        int64_t best_waste = -1;
+        const int64_t n0 = (Rs + max_rows - 1) / max_rows;
+        for (int64_t c = n0; c <= n0 + 4; ++c) {
+            int64_t rc = (Rs + c - 1) / c;
+            rc += rc & 1;
+            if (rc > max_rows) continue;
+            const int64_t waste = c * rc - Rs;
+            if (best_waste < 0 || waste < best_waste) { best_waste = waste; nch = (int)c; Rc = (int)rc; }
+        }
+        if (const char* e = getenv("ASY_SLAB_RC")) {  // debug override
+            Rc = std::max(2, std::min(256, atoi(e) & ~1));
+            nch = (int)((Rs + Rc - 1) / Rc);
+        }
+    }
+    const int64_t RsP = (Rs + 1) & ~1ll;
+    const int64_t stage_dbl = ((int64_t)Rc * BMAX + kSlabPad + 15) & ~15ll;
+    const size_t stage_bytes = sizeof(double) * stage_dbl;
+    const size_t fixed = sizeof(double) * (2 * RsP + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * BMAX + kSlabDot * 256) +
+                         sizeof(SeqMeta) * kSlabNM +
+                         sizeof(uint64_t) * (4 * kSlabMaxStages + 2 * kSlabNP + 2 * kSlabNDX) +
+                         sizeof(unsigned long long) * (kSlabAx + kSlabDot) + 128;
+    const size_t cap = 227 * 1024;
+    if (fixed + 3 * stage_bytes > cap) return h->fail(ASY_ERR_UNSUPPORTED, "row slab too tall for shared memory");
+    int total = (int)std::min<size_t>((cap - fixed) / stage_bytes, 2 * kSlabMaxStages);
+    // dot stages come in per-dot-warp sub-rings (kSlabDot of them).  Hold the chunks until
+    // the axpy when >= 2 sequences per dot warp fit, else re-load them from L2.
+    int hold = total / kSlabDot >= 2 * nch;
+    if (const char* e = getenv("ASY_SLAB_HOLD")) hold = atoi(e) != 0 && total / kSlabDot >= nch + 1;
+    int nst, nsa;
+    if (hold) {
+        nst = std::min(total, kSlabMaxStages) / kSlabDot * kSlabDot;
+        nsa = 0;
+    } else {
+        nsa = std::max(1, std::min(nch, total - kSlabDot));
+        if (total - nsa >= 2 * kSlabDot && nsa > 2) nsa = 2;
+        nst = std::min(total - nsa, kSlabMaxStages) / kSlabDot * kSlabDot;
+    }
+    if (nst < kSlabDot || (!hold && nsa < 1))
+        return h->fail(ASY_ERR_UNSUPPORTED, "row slab chunks too large for shared memory");
+    const size_t smem = fixed + stage_bytes * (nst + nsa);
+    // delay: the L2 must still hold a block between its dot pass and its re-load
+    if (!hold) {
+        const double blk_bytes = 8.0 * (double)m * (double)B;
+        const int64_t l2cap = std::max<int64_t>(1, (int64_t)(40e6 / blk_bytes));
+        delay = std::min(delay, l2cap);
+    }
+    delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
+    const int64_t slots = next_pow2(std::max<int64_t>(64, 2 * delay + 2));
+    const int det = delay == 0 ? 1 : 0;
+
+    SlabKernelFn fn = slab_kernel_for(cpw, h->S.loss);
+    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kSlabThreads, smem));
+    if (occ < 1) return h->fail(ASY_ERR_CUDA, "dense slab kernel does not fit on an SM");
+
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {(cuuint64_t)h->m, (cuuint64_t)h->n};
+    cuuint64_t strides[1] = {(cuuint64_t)(h->lda * sizeof(double))};
+    cuuint32_t box[2] = {(cuuint32_t)Rc, (cuuint32_t)B};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->A.p, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * B));
+    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
+    if (det) TRY(dev_alloc(h, h->dpart, sizeof(double) * slots * grid * B));
+
+    SlabParams P{};
+    P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk;
+    P.Rs = Rs; P.Rc = Rc; P.nch = nch; P.hold = hold; P.nst = nst; P.nsa = nsa; P.stage_dbl = stage_dbl;
+    P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
+    P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
+    P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
+    P.K = sweeps * h->nblk; P.delay = delay; P.deterministic = det;
+    P.gacc = P_<double>(h->gacc); P.part = det ? P_<double>(h->dpart) : nullptr; P.arrive = P_<unsigned>(h->arrive);
+    P.slots = slots;
+    const char* pf = getenv("ASY_PROF");
+    Dev prof;
+    if (pf) {
+        TRY(dev_alloc(h, prof, sizeof(unsigned long long) * grid * kSlabWarps * 8));
+        CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * grid * kSlabWarps * 8, h->stream));
+        P.prof = P_<unsigned long long>(prof);
+    }
+    if (getenv("ASY_SLAB_VERBOSE"))
+        fprintf(stderr, "[slab] grid %d Rs %lld Rc %d nch %d hold %d nst %d nsa %d smem %zu delay %lld slots %lld det %d\n",
+                grid, (long long)Rs, Rc, nch, hold, nst, nsa, smem, (long long)delay, (long long)slots, det);
+    slab_init<<<grid_for(2 * slots * B, 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    CKL();
+    void* args[] = {&tmap, &P};
+    CK(cudaEventRecord(h->ev[0], h->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kSlabThreads), args, smem, h->stream));
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventSynchronize(h->ev[1]));
+    CKL();
+    CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    if (sweeps & 1) std::swap(h->x, h->xalt);  // the updated iterate lives in the other half
+    if (P.prof) {
+        std::vector<unsigned long long> hb((size_t)grid * kSlabWarps * 8);
+        CK(cudaMemcpy(hb.data(), prof.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
+        FILE* f = fopen(pf, "wb");
+        if (f) {
+            fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+            fclose(f);
+        }
+        dev_free(prof);
+    }
+    return ASY_OK;
+}
+
+// Which dense asynchronous kernel: the row-slab kernel when every SM's share of a block
+// update is large (>= 128 KB: tall and wide blocks, e.g. configs[3]); the TMEM panel
+// kernel otherwise (a block update touches only G of the SMs, no global all-reduce per
+// update).  ASY_DENSE_KERNEL=panel|slab overrides (tests, measurements).
+static bool use_slab_kernel(const asy_handle* h) {
+    if (const char* kv = getenv("ASY_DENSE_KERNEL")) {
+        if (!strcmp(kv, "panel")) return false;
+        if (!strcmp(kv, "slab")) return true;
+    }
+    const double per_sm = 8.0 * (double)h->B * (double)h->m / (double)std::max(1, h->sms);
+    return per_sm >= 128.0 * 1024.0;
+}
+
 static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
                                float* ms) {
     int occ = 0;
@@ -755,7 +924,10 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
             launches += chunk * (h->kind == ASY_DENSE_COLMAJOR ? 4 : 3);
         } else {
             float ms = 0;
-            if (h->kind == ASY_DENSE_COLMAJOR) TRY(dense_async_launch(h, sp, chunk, delay, &ms));
+            if (h->kind == ASY_DENSE_COLMAJOR) {
+                if (use_slab_kernel(h)) TRY(dense_slab_launch(h, sp, chunk, delay, &ms));
+                else TRY(dense_async_launch(h, sp, chunk, delay, &ms));
+            }
             else TRY(sparse_async_launch(h, sp, chunk, delay, &ms));
             kernel_ms += ms;
             launches += 2;

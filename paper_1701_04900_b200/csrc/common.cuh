@@ -82,6 +82,39 @@ ASY_HD int64_t schedule_block(int sched, uint64_t seed, int64_t nblocks, int64_t
     return (int64_t)v;
 }
 
+// inverse of one Feistel pass: round r maps (L, R) -> (R, L ^ F_r(R))
+ASY_HD uint64_t feistel_inv(uint64_t v, int half, const PermKeys& pk) {
+    const uint64_t mask = ((uint64_t)1 << half) - 1;
+    uint64_t L = v >> half, R = v & mask;
+#pragma unroll
+    for (int r = 3; r >= 0; --r) {
+        const uint64_t F = (uint64_t)fmix32((uint32_t)L ^ pk.k[r] ^ (uint32_t)(L >> 32)) & mask;
+        const uint64_t oL = R ^ F;
+        R = L;
+        L = oL;
+    }
+    return (L << half) | R;
+}
+
+// position of block b in epoch e's order (inverse of schedule_block within the
+// epoch; cycle-walking inverts the same way it permutes)
+ASY_HD int64_t schedule_position(int sched, uint64_t seed, int64_t nblocks, int64_t e, int64_t b) {
+    if (sched == SCHED_CYCLIC) return b;
+    const PermKeys pk = perm_keys(seed, e);
+    const int half = perm_half_bits(nblocks);
+    uint64_t v = (uint64_t)b;
+    do { v = feistel_inv(v, half, pk); } while (v >= (uint64_t)nblocks);
+    return (int64_t)v;
+}
+
+// global index of the previous update of the block that sequence k updates
+// (-1: none).  Every epoch visits each block once, so it lies in epoch e-1.
+ASY_HD int64_t schedule_prev(int sched, uint64_t seed, int64_t nblocks, int64_t k, int64_t b) {
+    const int64_t e = k / nblocks;
+    if (e == 0) return -1;
+    return (e - 1) * nblocks + schedule_position(sched, seed, nblocks, e - 1, b);
+}
+
 // ---------------------------------------------------------------------------
 // the problem's scalar maps
 // ---------------------------------------------------------------------------
@@ -99,12 +132,16 @@ struct Scalars {
 };
 
 // w_j = phi_j'(r_j): grad f = A^T w (- 2c x).  LS: r = Ax-b, w = 2s r.
-// Logistic: r = z = Ax, w = -(y/m) sigmoid(-y z).
-ASY_HD double loss_prime(const Scalars& S, double r, double aux) {
-    if (S.loss == LOSS_LS) return S.s2 * r;
+// Logistic: r = z = Ax, w = -(y/m) sigmoid(-y z).  (LOSS fixed at compile time.)
+template <int LOSS>
+ASY_HD double loss_prime_t(const Scalars& S, double r, double aux) {
+    if (LOSS == LOSS_LS) return S.s2 * r;
     const double t = -aux * r;  // sigmoid(t)
     const double sig = t >= 0.0 ? 1.0 / (1.0 + exp(-t)) : exp(t) / (1.0 + exp(t));
     return -aux * S.minv * sig;
+}
+ASY_HD double loss_prime(const Scalars& S, double r, double aux) {
+    return S.loss == LOSS_LS ? loss_prime_t<LOSS_LS>(S, r, aux) : loss_prime_t<LOSS_LOGISTIC>(S, r, aux);
 }
 
 // phi_j(r_j): LS: s r^2 (= s2/2 r^2); logistic: (1/m) log(1+exp(-y z)).

@@ -193,6 +193,13 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void spin_until_ge_relaxed(const unsigned* p, unsigned v) {
+    unsigned ns = 32;
+    while (ld_relaxed_u32(p) < v) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+}
 
 // ---- TMEM (tcgen05) ---------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc_512(uint32_t* dst_smem) {
@@ -414,9 +421,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const unsigned need_s = (unsigned)(k / P.slots) * G;            // seq k - S complete
                     const unsigned need_w = kd >= 0 ? (unsigned)(kd / P.slots + 1) * G : 0u;  // seq kd complete
                     if (xv[i] < need_x || cs[i] < need_s || cw[i] < need_w) {
-                        spin_until_ge_u32(&P.xver[e[i].b], need_x);
-                        spin_until_ge_u32(&P.consumed[k & (P.slots - 1)], need_s);
-                        if (kd >= 0) spin_until_ge_u32(&P.consumed[kd & (P.slots - 1)], need_w);
+                        // relaxed polls (ld.acquire would invalidate the SM's L1 on every poll),
+                        // then one fence: acquire for everything the TMA loads next
+                        spin_until_ge_relaxed(&P.xver[e[i].b], need_x);
+                        spin_until_ge_relaxed(&P.consumed[k & (P.slots - 1)], need_s);
+                        if (kd >= 0) spin_until_ge_relaxed(&P.consumed[kd & (P.slots - 1)], need_w);
+                        fence_acqrel_gpu();
+                        fenced = true;
                     } else if (!fenced) {
                         fence_acqrel_gpu();
                         fenced = true;
@@ -628,11 +639,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             {
                 const unsigned need = (unsigned)((use + 1) * P.G);
                 unsigned ok = 0;
-                if (lane == 0) ok = ld_acquire_u32(&P.arrive[slot]) >= need;
+                // relaxed poll: everything read after it that other SMs wrote (accumulator, x) is
+                // read with strong L2 loads, so no L1 invalidation (acquire) is needed
+                if (lane == 0) ok = ld_relaxed_u32(&P.arrive[slot]) >= need;
                 ok = __shfl_sync(0xffffffffu, ok, 0);
                 if (!ok) {
                     complete();
-                    if (lane == 0) spin_until_ge_u32(&P.arrive[slot], need);
+                    if (lane == 0) spin_until_ge_relaxed(&P.arrive[slot], need);
                 }
             }
             __syncwarp();

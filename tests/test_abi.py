@@ -58,6 +58,21 @@ def test_schedule_matches_oracle_and_is_permutation(lib, nblocks):
         list(range(nblocks)) * 2
 
 
+@pytest.mark.parametrize("sched", ["cyclic", "random"])
+@pytest.mark.parametrize("nblocks", [1, 5, 64, 625])
+def test_schedule_prev_is_previous_occurrence(lib, sched, nblocks):
+    """asy_schedule_prev (the D4 guard of the dense kernel) against a brute-force scan
+    of the oracle's schedule: the last earlier sequence that updated the same block."""
+    sc = lib.ASY_SCHED_CYCLIC if sched == "cyclic" else lib.ASY_SCHED_RANDOM
+    for seed in (0, 99):
+        order = (O.cyclic_schedule(nblocks, 3) if sched == "cyclic"
+                 else [b for e in range(3) for b in O.random_epoch_order(seed, e, nblocks)])
+        last = {}
+        for k, b in enumerate(order):
+            assert lib.asy_schedule_prev(sc, seed, nblocks, k) == last.get(b, -1)
+            last[b] = k
+
+
 def test_random_epochs_differ(lib):
     a = O.random_epoch_order(1, 0, 500)
     b = O.random_epoch_order(1, 1, 500)

@@ -225,11 +225,22 @@ def test_async_long_launch_slot_reuse_ragged(A):
         S.close()
 
 
+DENSE_VARIANTS = {
+    "slab_hold": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_HOLD": "1"},   # axpy reads the dot pass's chunk
+    "slab_reload": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_HOLD": "0"},  # axpy re-loads the chunk (L2)
+    "slab_chunks": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_RC": "8"},    # many chunks per sequence
+    "panel": {"ASY_DENSE_KERNEL": "panel"},           # TMEM panel kernel
+    "panel_reread": {"ASY_DENSE_KERNEL": "panel", "ASY_NO_TMEM": "1"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(DENSE_VARIANTS))
 @pytest.mark.parametrize("case", ["dense_ragged", "large_block", "nonconvex"])
-def test_reread_path_parity(A, case, monkeypatch):
-    """Panels that are not parked in TMEM are re-read from HBM/L2 by the axpy warps;
-    force that path (ASY_NO_TMEM) and check sequential parity and async convergence."""
-    monkeypatch.setenv("ASY_NO_TMEM", "1")
+def test_dense_kernel_variants(A, case, variant, monkeypatch):
+    """Every geometry / code path of the dense asynchronous kernels: sequential parity
+    (per iteration) and asynchronous convergence to the oracle's solution."""
+    for k, v in DENSE_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
     P = make_case(case)
     S = A.Solver(P)
     try:
@@ -239,12 +250,31 @@ def test_reread_path_parity(A, case, monkeypatch):
         x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
         S.solve(sweeps=0, reset=True)
         for _ in range(60):
-            S.solve(sweeps=100)
+            S.solve(sweeps=100, schedule=A.ASY_SCHED_RANDOM, seed=5)
             out = S.stationarity()
             meas = out.merit_inf if P.c > 0 else out.mf_norm2
             if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
                 break
         assert _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("kernel", ["slab", "panel"])
+@pytest.mark.parametrize("workers", [1, 3, 37])
+def test_dense_few_workers(A, workers, kernel, monkeypatch):
+    """Fewer CTAs than SMs (taller row slabs / fewer panel workers), same results."""
+    monkeypatch.setenv("ASY_DENSE_KERNEL", kernel)
+    P = make_case("dense_ragged")
+    S = A.Solver(P)
+    try:
+        S.solve(sweeps=3, max_delay=0, reset=True, workers=workers)
+        x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 3))
+        assert _rel_x(S.x(), x_or) <= REL
+        S.solve(sweeps=200, reset=True, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=1)
+        x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
+        out = S.stationarity()
+        assert _rel_f(out.objective, F_star) <= 1e-6 and out.mf_norm2 <= 1e-5
     finally:
         S.close()
 
