@@ -17,6 +17,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libasyflexa.so")
+if os.environ.get("ASY_LIB_VARIANT"):  # developer builds with other compile-time geometry (tools/)
+    LIB_PATH = os.path.join(_HERE, "lib", "libasyflexa_%s.so" % os.environ["ASY_LIB_VARIANT"])
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1701_04900_b200.build` "
                       "(there is no CPU fallback)")

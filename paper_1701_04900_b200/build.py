@@ -26,6 +26,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Developer build with extra -D flags -> lib/libasyflexa_<name>.so (ASY_LIB_VARIANT=name)."""
+    out = os.path.join(HERE, "lib", "libasyflexa_%s.so" % name)
+    cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-o", out, SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
@@ -43,4 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":  # --variant NAME DEF [DEF ...]
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

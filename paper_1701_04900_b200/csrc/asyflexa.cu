@@ -649,6 +649,8 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
     P.xver = P_<unsigned>(h->ver);
     P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad;
+    P.lg_slots = 0;
+    while (((int64_t)1 << P.lg_slots) < slots) ++P.lg_slots;
 
     // debug trace (env ASY_TRACE=<subtasks>, ASY_TRACE_FILE=<path>): globaltimer stamps per subtask
     const char* tr = getenv("ASY_TRACE");

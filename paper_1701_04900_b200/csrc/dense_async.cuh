@@ -59,15 +59,25 @@
 namespace asy {
 
 constexpr int kPairs = 4;
-constexpr int kAxpyPerPair = 1;
+#ifndef ASY_AXPY_PER_PAIR
+#define ASY_AXPY_PER_PAIR 1
+#endif
+constexpr int kAxpyPerPair = ASY_AXPY_PER_PAIR;  // axpy warps per pair (2: hand-offs alternate)
 constexpr int kTmemSlots = 2;        // parked panels per pair (TMEM lane quarter = 2 x 256 columns)
-constexpr int kProducerWarp = 8;
-constexpr int kSchedWarp = 9;
-constexpr int kDenseThreads = 32 * 10;
-constexpr int kQueue = 4;            // scheduler -> producer queue depth
+constexpr int kProducerWarp = kPairs * (1 + kAxpyPerPair);  // after axpy (0-3[, 8-11]) and dot (4-7)
+constexpr int kSchedWarp = kProducerWarp + 1;
+constexpr int kDenseThreads = 32 * (kSchedWarp + 1);
+constexpr int kSlotsPerAx = 2 / kAxpyPerPair;  // TMEM slots owned by each axpy warp
+#ifndef ASY_QUEUE
+#define ASY_QUEUE 2
+#endif
+#ifndef ASY_CLAIM
+#define ASY_CLAIM 4
+#endif
+constexpr int kQueue = ASY_QUEUE;    // scheduler -> producer queue depth
 constexpr int kRing = 32;            // hand-off notes per axpy warp
 constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
-constexpr int kClaim = 4;            // subtasks claimed per atomic
+constexpr int kClaim = ASY_CLAIM;    // subtasks claimed per atomic
 constexpr int kSlotCols = 256;       // TMEM columns per parked panel
 constexpr unsigned long long kParkWaitNs = 20000;  // max wait for a TMEM slot before re-reading
 
@@ -102,6 +112,7 @@ struct DenseAsyncParams {
     unsigned* consumed;  // [S]        monotonic: completed panels of all users of the slot
     unsigned* xver;      // [nblk]     monotonic: completed panels of all updates of block b
     int64_t slots;       // power of two
+    int lg_slots;        // log2(slots)
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
     unsigned long long* prof;   // optional [grid][warps][8] clock64 segment sums (debug; null = off)
@@ -122,6 +133,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 struct StageMeta {
     long long t, k, b, p;
+    long long u;  // local epoch of sequence k (k / N): x double buffer, D4 guard
 };
 
 // clock64 segment profiler (debug): seg[i] += cycles since the previous mark
@@ -388,55 +400,78 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 mbar_arrive(&qfull[qs]);
                 ++qi;
             };
-            for (;;) {
-                const long long tb = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
-                if (tb >= P.T) break;
+            // Per batch: claim kClaim subtasks, evaluate the schedule (once per sequence, the
+            // permutation keys once per epoch), check the guards, queue them.  The next claim's
+            // atomic is issued before this batch is processed so its round trip overlaps.
+            const long long G = P.G, N = P.nblk;
+            const int lgS = P.lg_slots;
+            const int half = perm_half_bits(N);
+            PermKeys pk{};
+            long long ck = -1, cb = 0, cu = 0, cE = -1;  // cached sequence / block / epochs
+            long long tb = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
+            while (tb < P.T) {
+                const long long tn = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
                 StageMeta e[kClaim];
                 unsigned xv[kClaim], cs[kClaim], cw[kClaim];
+                long long k = tb / G, p = tb - k * G;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long t = tb + i;
+                    if (k != ck) {
+                        ck = k;
+                        cu = k / N;
+                        const long long pos = k - cu * N;
+                        cb = pos;
+                        if (P.sched == SCHED_RANDOM) {
+                            const long long E = P.epoch0 + cu;
+                            if (E != cE) { pk = perm_keys(P.seed, E); cE = E; }
+                            uint64_t v = (uint64_t)pos;
+                            do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
+                            cb = (long long)v;
+                        }
+                    }
                     e[i].t = t < P.T ? t : -1;
-                    e[i].k = t / P.G;
-                    e[i].p = t - e[i].k * P.G;
-                    e[i].b = schedule_block(P.sched, P.seed, P.nblk, P.epoch0 * P.nblk + e[i].k);
+                    e[i].k = k;
+                    e[i].p = p;
+                    e[i].b = cb;
+                    e[i].u = cu;
                     ASY_TRACE(P, t, 0);
+                    if (++p == G) { p = 0; ++k; }
                 }
                 // guards: all loads in flight at once
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
-                    const long long k = e[i].k, kd = k - P.delay - 1;
+                    const long long kk = e[i].k, kd = kk - P.delay - 1;
                     xv[i] = ld_relaxed_u32(&P.xver[e[i].b]);
-                    cs[i] = ld_relaxed_u32(&P.consumed[k & (P.slots - 1)]);
+                    cs[i] = ld_relaxed_u32(&P.consumed[kk & (P.slots - 1)]);
                     cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[kd & (P.slots - 1)]) : 0u;
                 }
-                // admit in claim order: a subtask never waits while an older one of this batch is held back
-                bool fenced = false;
+                // admit in claim order: a subtask never waits while an older one of this batch is
+                // held back.  Guards are observed with relaxed loads: the TMA reads residual rows
+                // and A from L2 (never through L1), and the counters were released (after a fence)
+                // by the SMs that completed the updates, so nothing stale can be read; a fence
+                // follows only a guard that had to wait.
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     if (e[i].t < 0) continue;
-                    const long long k = e[i].k, kd = k - P.delay - 1;
-                    const unsigned G = (unsigned)P.G;
-                    const unsigned need_x = (unsigned)(k / P.nblk) * G;             // previous update of b
-                    const unsigned need_s = (unsigned)(k / P.slots) * G;            // seq k - S complete
-                    const unsigned need_w = kd >= 0 ? (unsigned)(kd / P.slots + 1) * G : 0u;  // seq kd complete
+                    const long long kk = e[i].k, kd = kk - P.delay - 1;
+                    const unsigned Gu = (unsigned)G;
+                    const unsigned need_x = (unsigned)e[i].u * Gu;                         // previous update of b
+                    const unsigned need_s = (unsigned)(kk >> lgS) * Gu;                    // seq k - S complete
+                    const unsigned need_w = kd >= 0 ? (unsigned)((kd >> lgS) + 1) * Gu : 0u;  // seq kd complete
                     if (xv[i] < need_x || cs[i] < need_s || cw[i] < need_w) {
-                        // relaxed polls (ld.acquire would invalidate the SM's L1 on every poll),
-                        // then one fence: acquire for everything the TMA loads next
+                        // relaxed polls (ld.acquire would invalidate the SM's L1 on every poll)
                         spin_until_ge_relaxed(&P.xver[e[i].b], need_x);
-                        spin_until_ge_relaxed(&P.consumed[k & (P.slots - 1)], need_s);
+                        spin_until_ge_relaxed(&P.consumed[kk & (P.slots - 1)], need_s);
                         if (kd >= 0) spin_until_ge_relaxed(&P.consumed[kd & (P.slots - 1)], need_w);
                         fence_acqrel_gpu();
-                        fenced = true;
-                    } else if (!fenced) {
-                        fence_acqrel_gpu();
-                        fenced = true;
                     }
                     push(e[i]);
                 }
+                tb = tn;
             }
             StageMeta end;
-            end.t = -1; end.k = end.b = end.p = 0;
+            end.t = -1; end.k = end.b = end.p = end.u = 0;
             push(end);
         }
         __syncwarp();
@@ -444,35 +479,43 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         // ------------------------------------------------------------------ dot warps
         const int q = warp - kPairs;
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * q) << 16);
-        unsigned tm_used = 0u;  // panels parked by this pair so far (slot = tm_used % kTmemSlots)
+        static_assert(kSlotsPerAx * kAxpyPerPair == kTmemSlots, "axpy warp h owns TMEM slots h*kSlotsPerAx..");
+        unsigned tm_used0 = 0u, tm_used1 = 0u;  // panels parked for the pair's axpy warp h = 0 / 1
         SegProf sp;
         sp.start();
         for (long long j = 0;; ++j) {
             const long long it = j * kPairs + q;  // pair q owns stage q
             const int st = (int)(it % NS);
-            const int h = 0;                                   // one axpy warp per pair
-            const int ax = q;                                  // its warp id
-            const long long e = j;                             // its ring position
+            const int h = kAxpyPerPair == 2 ? (int)(j & 1) : 0;  // hand-offs alternate between them
+            const int ax = q * kAxpyPerPair + h;                  // axpy warps of the pair
+            const long long e = j / kAxpyPerPair;                 // ring position of axpy warp ax
             const int rs = (int)(e % kRing);
-            Handoff* ho = &ring[(q * kAxpyPerPair + h) * kRing + rs];
-            uint64_t* rf = &rfull[(q * kAxpyPerPair + h) * kRing + rs];
-            uint64_t* re = &rempty[(q * kAxpyPerPair + h) * kRing + rs];
+            Handoff* ho = &ring[ax * kRing + rs];
+            uint64_t* rf = &rfull[ax * kRing + rs];
+            uint64_t* re = &rempty[ax * kRing + rs];
+            unsigned tm_used = h ? tm_used1 : tm_used0;
             mbar_wait(&full[st], (uint32_t)((it / NS) & 1));
             sp.mark(0);
             const StageMeta md = meta[st];
             if (md.t < 0) {
                 if (lane == 0) mbar_arrive(&empty[st]);
-                // end marker for the pair's axpy warp
-                if (e >= kRing) mbar_wait(re, (uint32_t)(((e / kRing) - 1) & 1));
-                if (lane == 0) {
-                    ho->md.t = -1;
-                    mbar_arrive(rf);
+                // end markers for both axpy warps of the pair (ring positions e and j - e)
+#pragma unroll
+                for (int hh = 0; hh < kAxpyPerPair; ++hh) {
+                    const long long eh = hh == h ? e : (j + 1 - hh) / kAxpyPerPair;
+                    const int rsh = (int)(eh % kRing);
+                    const int axh = q * kAxpyPerPair + hh;
+                    if (eh >= kRing) mbar_wait(&rempty[axh * kRing + rsh], (uint32_t)(((eh / kRing) - 1) & 1));
+                    if (lane == 0) {
+                        ring[axh * kRing + rsh].md.t = -1;
+                        mbar_arrive(&rfull[axh * kRing + rsh]);
+                    }
                 }
                 break;
             }
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
-            double* gacc = P.gacc + (slot * 2 + ((k / P.slots) & 1)) * Bmax;
+            double* gacc = P.gacc + (slot * 2 + ((k >> P.lg_slots) & 1)) * Bmax;
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const double* pan = stages + st * STAGE;
@@ -491,11 +534,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             int parked = 0;
             if (P.use_tmem) {
                 unsigned ok = 0;
-                if (lane == 0) ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                if (lane == 0) ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kSlotsPerAx;
                 parked = __shfl_sync(0xffffffffu, ok, 0);
                 if (parked) tc_fence_after();
             }
-            const int tslot_idx = (int)(tm_used % kTmemSlots);
+            const int tslot_idx = h * kSlotsPerAx + (int)(tm_used % kSlotsPerAx);
             const uint32_t tslot = tlane + (uint32_t)(tslot_idx * kSlotCols);
 #pragma unroll
             for (int g0 = 0; g0 < BT; g0 += GW) {
@@ -535,7 +578,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const unsigned long long t0 = gtimer();
                     do {
                         __nanosleep(64);
-                        ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kTmemSlots;
+                        ok = tm_used - ld_acquire_cta_u32(&tm_done[ax]) < (unsigned)kSlotsPerAx;
                     } while (!ok && gtimer() - t0 < kParkWaitNs);
                 }
                 parked = __shfl_sync(0xffffffffu, ok, 0);
@@ -559,7 +602,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 }
             }
             if (parked) {
-                ++tm_used;
+                if (h) ++tm_used1;
+                else ++tm_used0;
                 tmem_wait_st();
                 tc_fence_before();
             }
@@ -580,13 +624,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * 16 + warp) * 8 : nullptr, lane);
     } else {
         // ------------------------------------------------------------------ axpy warps
-        const int q = warp, h = 0;
-        const int ax = warp;
+        const int q = warp & 3, h = warp / (2 * kPairs);  // warps 0-3: h = 0, warps 8-11: h = 1
+        const int ax = q * kAxpyPerPair + h;
         const uint32_t tquarter = tmem_base + ((uint32_t)(32 * q) << 16);
-        double* dv = dxs + (q * kAxpyPerPair + h) * Bpad;
-        Handoff* myring = ring + (q * kAxpyPerPair + h) * kRing;
-        uint64_t* myfull = rfull + (q * kAxpyPerPair + h) * kRing;
-        uint64_t* myempty = rempty + (q * kAxpyPerPair + h) * kRing;
+        double* dv = dxs + ax * Bpad;
+        Handoff* myring = ring + ax * kRing;
+        uint64_t* myfull = rfull + ax * kRing;
+        uint64_t* myempty = rempty + ax * kRing;
         unsigned tm_fin = 0;
         long long pend_slot = -1, pend_b = -1;  // completion of the previous panel, issued late
         auto complete = [&]() {
@@ -615,12 +659,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             if (md.t < 0) break;
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
-            const long long use = k / P.slots;
+            const long long use = k >> P.lg_slots;
             const double* gacc = P.gacc + (slot * 2 + (use & 1)) * Bmax;
             double* gnext = P.gacc + (slot * 2 + ((use + 1) & 1)) * Bmax;
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
-            const long long u = k / P.nblk;
+            const long long u = md.u;
             const double* xr = (u & 1) ? P.x1 : P.x0;
             double* xw = (u & 1) ? P.x0 : P.x1;
             ASY_TRACE(P, md.t, 5);
@@ -651,23 +695,32 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             __syncwarp();
             ASY_TRACE(P, md.t, 6);
             sp.mark(1);
-            // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block
+            // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block.
+            // The accumulated gradient is loaded first; the previous panel's completion (a fence
+            // that waits for its residual red.adds) is issued while those loads are in flight.
+            double gv[(128 + 31) / 32];
+#pragma unroll
+            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+                const int c = lane + 32 * s4;
+                gv[s4] = 0.0;
+                if (c < nc) {
+                    if (P.deterministic) {
+                        for (long long qq = 0; qq < P.G; ++qq) gv[s4] += ld_relaxed_f64(&P.part[qq * Bmax + c]);
+                    } else {
+                        gv[s4] = ld_relaxed_f64(&gacc[c]);
+                    }
+                }
+            }
+            complete();
             bool nz = false;
 #pragma unroll
             for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
                 const int c = lane + 32 * s4;
                 double dd = 0.0;
                 if (c < nc) {
-                    double g;
-                    if (P.deterministic) {
-                        g = 0.0;
-                        for (long long qq = 0; qq < P.G; ++qq) g += ld_relaxed_f64(&P.part[qq * Bmax + c]);
-                    } else {
-                        g = ld_relaxed_f64(&gacc[c]);
-                    }
                     const long long jj = c0 + c;
                     const double y = ypre[s4];
-                    const double xh = best_response(P.S, g, y, tpre[s4], jj);
+                    const double xh = best_response(P.S, gv[s4], y, tpre[s4], jj);
                     const double xn = y + P.gamma * (xh - y);
                     xw[jj] = xn;  // every panel writes the same value
                     dd = xn - y;
@@ -681,9 +734,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             nz = __any_sync(0xffffffffu, nz);
             __syncwarp();
             sp.mark(2);
-            // the previous panel's completion: its red.adds were issued a whole panel ago, so this
-            // fence rarely waits (issued after this panel's red.adds it always would)
-            complete();
             sp.mark(3);
             ASY_TRACE(P, md.t, 8);
             const long long r0 = p * R;
