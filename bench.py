@@ -218,7 +218,7 @@ def run_ours(args, rank, world, local):
                 break
             st = S.solve(sweeps=args.check_every, **kw)
         stat = S.stationarity()
-        return updates, launches + 6, kms, sweeps, stat
+        return updates, launches + 6, kms, sweeps, stat, st.kernel, st.delay
 
     for _ in range(args.warmup):
         solve_to_target({})
@@ -314,8 +314,8 @@ def run_ours(args, rank, world, local):
                        "l2": "inputs larger than L2 (A = %.2f GB vs 126 MB)" % (bytes_per_sweep(P) / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "kernel": "asy::dense_async_kernel" if P.kind == "dense"
-                         else "asy::sparse_async_kernel",
+                         "traffic": traffic, "kernel": A.KERNEL_NAMES.get(res[-1][5], "?"),
+                         "enforced_delay": res[-1][6],
                          "bytes_per_sweep": bytes_per_sweep(P), "kernel_ms": kernel_ms / args.steps},
             "final": {"rel_err": (res[-1][4].objective - Fstar) / abs(Fstar), "mf_norm2": last_stat.mf_norm2,
                       "merit_inf": last_stat.merit_inf, "Fstar": Fstar, "Fstar_mf_norm2": st_star.mf_norm2},

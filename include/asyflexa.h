@@ -74,6 +74,12 @@ extern "C" {
 #define ASY_MODE_SYNC_JACOBI 1  /* deterministic synchronous Jacobi sweep x+ = x + gamma(hat x(x) - x)
                                    from two GEMVs (A^T w, then A dx) */
 
+/* update kernels (asy_solve_stats.kernel) */
+#define ASY_KERNEL_JACOBI 0      /* two GEMVs per sweep */
+#define ASY_KERNEL_DENSE_PANEL 1 /* dense_async.cuh: G row panels of a block on G SMs, TMEM parking */
+#define ASY_KERNEL_DENSE_SLAB 2  /* dense_slab.cuh: every SM owns a row slab, per-update all-reduce */
+#define ASY_KERNEL_SPARSE 3      /* sparse_async.cuh: CSC column updates */
+
 /* block schedules (S.1) [PAPER.md:253] */
 #define ASY_SCHED_CYCLIC 0  /* sequence k updates block k mod N */
 #define ASY_SCHED_RANDOM 1  /* sequence k updates block pi_e(k mod N), e = epoch, pi_e a
@@ -137,6 +143,9 @@ typedef struct {
     double total_ms;         /* device time of the whole call */
     double objective;        /* F(x) at return, from the maintained residual */
     int64_t epochs;          /* cumulative sweeps since the last reset */
+    int32_t kernel;          /* update kernel of the last launch: ASY_KERNEL_* */
+    int32_t delay;           /* async: bounded delay actually enforced (<= max_delay; capped by the
+                                kernel's buffering), -1 for Jacobi */
 } asy_solve_stats;
 
 typedef struct {

@@ -32,6 +32,9 @@ ASY_LOSS_LS, ASY_LOSS_LOGISTIC = 0, 1
 ASY_REG_L1, ASY_REG_EXP, ASY_REG_LOG = 0, 1, 2
 ASY_MODE_ASYNC, ASY_MODE_SYNC_JACOBI = 0, 1
 ASY_SCHED_CYCLIC, ASY_SCHED_RANDOM = 0, 1
+ASY_KERNEL_JACOBI, ASY_KERNEL_DENSE_PANEL, ASY_KERNEL_DENSE_SLAB, ASY_KERNEL_SPARSE = 0, 1, 2, 3
+KERNEL_NAMES = {0: "jacobi (asy::dense_gemvT/gemvN)", 1: "asy::dense_async_kernel",
+                2: "asy::dense_slab_kernel", 3: "asy::sparse_async_kernel"}
 
 _vp, _dp = C.c_void_p, C.POINTER(C.c_double)
 
@@ -56,7 +59,8 @@ class asy_solve_params(C.Structure):
 
 class asy_solve_stats(C.Structure):
     _fields_ = [("block_updates", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double),
-                ("total_ms", C.c_double), ("objective", C.c_double), ("epochs", C.c_int64)]
+                ("total_ms", C.c_double), ("objective", C.c_double), ("epochs", C.c_int64),
+                ("kernel", C.c_int32), ("delay", C.c_int32)]
 
 
 class asy_stationarity_out(C.Structure):

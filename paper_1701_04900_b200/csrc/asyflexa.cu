@@ -60,6 +60,7 @@ struct asy_handle {
     Dev counter, gacc, dpart, arrive, consumed, done, ver;
     int64_t slots = 0;
     int64_t epochs = 0;                   // sweeps since reset (schedule epoch)
+    int last_kernel = 0, last_delay = -1; // reported in asy_solve_stats
 
     int fail(int code, const char* fmt, ...) {
         char buf[512];
@@ -557,10 +558,12 @@ struct DenseGeom {
 // compiled (BT, RPL) instantiations of dense_async_kernel: BT = block width padded to
 // {8,16,32,64,128}, RPL = panel rows per lane; default R*BT = 4096 doubles (32 KB panels)
 using DenseKernelFn = void (*)(const CUtensorMap, const DenseAsyncParams);
-static DenseKernelFn dense_kernel_for(int BT, int RPL, int NS) {
-#define ASY_DK(bt, rpl, ns) if (BT == bt && RPL == rpl && NS == ns) return dense_async_kernel<bt, rpl, ns>;
-    ASY_DK(8, 8, 4) ASY_DK(8, 4, 8) ASY_DK(16, 8, 4) ASY_DK(16, 4, 8) ASY_DK(32, 4, 4) ASY_DK(32, 3, 8)
-    ASY_DK(32, 2, 8) ASY_DK(64, 2, 4) ASY_DK(64, 1, 8) ASY_DK(128, 1, 4)
+static DenseKernelFn dense_kernel_for(int BT, int RPL, int NS, int loss) {
+#define ASY_DK(bt, rpl, ns)                                                                   \
+    if (BT == bt && RPL == rpl && NS == ns)                                                   \
+        return loss == LOSS_LS ? dense_async_kernel<bt, rpl, ns, LOSS_LS>                     \
+                               : dense_async_kernel<bt, rpl, ns, LOSS_LOGISTIC>;
+    ASY_DK(8, 8, 4) ASY_DK(16, 8, 4) ASY_DK(32, 4, 4) ASY_DK(32, 2, 8) ASY_DK(64, 2, 4) ASY_DK(128, 1, 4)
 #undef ASY_DK
     return nullptr;
 }
@@ -577,12 +580,12 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     if (getenv("ASY_DENSE_NS")) NS = atoi(getenv("ASY_DENSE_NS"));
     if (sp->panel_rows > 0) {
         const int want = sp->panel_rows / 32;
-        if (dense_kernel_for(BT, want, NS)) RPL = want;
-        else if (dense_kernel_for(BT, want, kPairs)) { RPL = want; NS = kPairs; }
+        if (dense_kernel_for(BT, want, NS, h->S.loss)) RPL = want;
+        else if (dense_kernel_for(BT, want, kPairs, h->S.loss)) { RPL = want; NS = kPairs; }
     }
     const int64_t R = 32 * RPL;
     const int64_t G = (h->m + R - 1) / R;
-    DenseKernelFn fn = dense_kernel_for(BT, RPL, NS);
+    DenseKernelFn fn = dense_kernel_for(BT, RPL, NS, h->S.loss);
     if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no dense kernel for BT=%d RPL=%d NS=%d", BT, RPL, NS);
     int use_tmem = RPL * 2 * BT <= kSlotCols;
     if (getenv("ASY_NO_TMEM")) use_tmem = 0;  // debug/test: force the re-read path
@@ -644,6 +647,8 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
     delay = geo.delay;
+    h->last_kernel = ASY_KERNEL_DENSE_PANEL;
+    h->last_delay = (int)delay;
     P.T = sweeps * h->nblk * G; P.delay = delay; P.deterministic = delay == 0 ? 1 : 0;
     P.counter = P_<unsigned long long>(h->counter); P.gacc = P_<double>(h->gacc);
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
@@ -785,6 +790,8 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
     const int64_t slots = next_pow2(std::max<int64_t>(64, 2 * delay + 2));
     const int det = delay == 0 ? 1 : 0;
+    h->last_kernel = ASY_KERNEL_DENSE_SLAB;
+    h->last_delay = (int)delay;
 
     SlabKernelFn fn = slab_kernel_for(cpw, h->S.loss);
     CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -879,6 +886,8 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     P.epoch0 = h->epochs; P.K = sweeps * h->n; P.delay = delay; P.counter = P_<unsigned long long>(h->counter);
     P.ver = P_<unsigned>(h->ver); P.done = P_<long long>(h->done); P.slots = slots;
     P.chunk = delay == 0 ? 4 : 32;
+    h->last_kernel = ASY_KERNEL_SPARSE;
+    h->last_delay = (int)delay;
     sparse_async_init<<<grid_for(std::max<int64_t>(slots, h->n), 256, 8 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
     void* args[] = {&P};
@@ -918,6 +927,8 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
         if (sp->mode == ASY_MODE_SYNC_JACOBI) {
             cudaEventRecord(h->ev[0], h->stream);
             for (int64_t s = 0; s < chunk; ++s) TRY(jacobi_sweep(h, sp->gamma));
+            h->last_kernel = ASY_KERNEL_JACOBI;
+            h->last_delay = -1;
             cudaEventRecord(h->ev[1], h->stream);
             CK(cudaEventSynchronize(h->ev[1]));
             float ms = 0;
@@ -961,6 +972,8 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     stats.total_ms = tot;
     stats.launches = launches;
     stats.epochs = h->epochs;
+    stats.kernel = h->last_kernel;
+    stats.delay = h->last_delay;
     if (st) *st = stats;
     return ASY_OK;
 }

@@ -153,12 +153,22 @@ ASY_HD double loss_value(const Scalars& S, double r, double aux) {
 }
 
 // d/dt h^-(t), h^- = eta|t| - h(t)  (Eq. 12 [PAPER.md:530]).
-ASY_HD double grad_h_minus(const Scalars& S, double t) {
-    if (S.reg == REG_L1) return 0.0;
+// (the DC branch is out of line on the device: it keeps exp/log1p out of the hot
+// loops' instruction footprint; l1 never calls it)
+#if defined(__CUDA_ARCH__)
+__device__ __noinline__
+#else
+inline
+#endif
+double grad_h_minus_dc(int reg, double eta, double theta, double t) {
     const double sg = t > 0.0 ? 1.0 : (t < 0.0 ? -1.0 : 0.0);
     const double a = fabs(t);
-    if (S.reg == REG_EXP) return S.eta * sg * (1.0 - exp(-S.theta * a));
-    return sg * (S.eta - S.theta / ((1.0 + S.theta * a) * log1p(S.theta)));
+    if (reg == REG_EXP) return eta * sg * (1.0 - exp(-theta * a));
+    return sg * (eta - theta / ((1.0 + theta * a) * log1p(theta)));
+}
+ASY_HD double grad_h_minus(const Scalars& S, double t) {
+    if (S.reg == REG_L1) return 0.0;
+    return grad_h_minus_dc(S.reg, S.eta, S.theta, t);
 }
 
 // h(t) of G = lambda sum h(x_j).

@@ -305,9 +305,10 @@ __device__ __forceinline__ double transpose_reduce8(double (&v)[8], int lane) {
 // a second stage per pair overlaps the next panel's load with this one's dot).
 // All compile-time so that the inner loops are fully unrolled with immediate
 // shared-memory offsets.
-template <int BT, int RPL, int NS>
+template <int BT, int RPL, int NS, int LOSS>
 __global__ void __launch_bounds__(kDenseThreads, 1)
     dense_async_kernel(const __grid_constant__ CUtensorMap tmap, const DenseAsyncParams P) {
+    constexpr int NPL = (BT + 31) / 32;  // block columns per lane in the solve
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     static_assert(NS % kPairs == 0, "pair q owns stages q (mod kPairs)");
     constexpr int NAX = kPairs * kAxpyPerPair;
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
             for (int qq = 0; qq < RPL; ++qq) {
                 const int i = lane + 32 * qq;
-                w[qq] = (r0 + i) < P.m ? loss_prime(P.S, rsm[i], rsm[R + i]) : 0.0;
+                w[qq] = (r0 + i) < P.m ? loss_prime_t<LOSS>(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
             sp.mark(1);
             // a free TMEM slot now?  then dot and park in ONE pass over shared memory
@@ -669,9 +670,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             double* xw = (u & 1) ? P.x0 : P.x1;
             ASY_TRACE(P, md.t, 5);
             // x_b (previous epoch, final by the D4 guard) and tau do not depend on the arrivals
-            double ypre[(128 + 31) / 32], tpre[(128 + 31) / 32];
+            double ypre[NPL], tpre[NPL];
 #pragma unroll
-            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+            for (int s4 = 0; s4 < NPL; ++s4) {
                 const int c = lane + 32 * s4;
                 // L2 read: another SM wrote this half of x in the previous epoch, and a line of it
                 // may still sit in this SM's (non-coherent) L1 from an older epoch
@@ -698,13 +699,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             // block subproblem (Eq. 2, closed form) + (S.4): identical in every panel of the block.
             // The accumulated gradient is loaded first; the previous panel's completion (a fence
             // that waits for its residual red.adds) is issued while those loads are in flight.
-            double gv[(128 + 31) / 32];
+            double gv[NPL];
 #pragma unroll
-            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+            for (int s4 = 0; s4 < NPL; ++s4) {
                 const int c = lane + 32 * s4;
                 gv[s4] = 0.0;
                 if (c < nc) {
                     if (P.deterministic) {
+#pragma unroll 1
                         for (long long qq = 0; qq < P.G; ++qq) gv[s4] += ld_relaxed_f64(&P.part[qq * Bmax + c]);
                     } else {
                         gv[s4] = ld_relaxed_f64(&gacc[c]);
@@ -714,7 +716,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             complete();
             bool nz = false;
 #pragma unroll
-            for (int s4 = 0; s4 < (128 + 31) / 32; ++s4) {
+            for (int s4 = 0; s4 < NPL; ++s4) {
                 const int c = lane + 32 * s4;
                 double dd = 0.0;
                 if (c < nc) {
