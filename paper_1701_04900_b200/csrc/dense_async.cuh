@@ -68,6 +68,10 @@ constexpr int kProducerWarp = kPairs * (1 + kAxpyPerPair);  // after axpy (0-3[,
 constexpr int kSchedWarp = kProducerWarp + 1;
 constexpr int kDenseThreads = 32 * (kSchedWarp + 1);
 constexpr int kSlotsPerAx = 2 / kAxpyPerPair;  // TMEM slots owned by each axpy warp
+#ifndef ASY_ROLL
+#define ASY_ROLL 1   // unroll factor of the per-lane row loops (1: rolled, small I-cache footprint)
+#endif
+constexpr int kRoll = ASY_ROLL;
 #ifndef ASY_QUEUE
 #define ASY_QUEUE 2
 #endif
@@ -348,7 +352,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_base_s;
-    constexpr int rows_per_lane = RPL;
     constexpr int cols_per_row = 2 * Bpad;  // b32 TMEM columns per panel row
 
     if (warp == kProducerWarp) {
@@ -520,15 +523,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const double* pan = stages + st * STAGE;
-            const double* rsm = pan + PANEL;
+            double* rsm = stages + st * STAGE + PANEL;
             ASY_TRACE(P, md.t, 2);
-            // w = phi'(r) on this lane's panel rows (residual and b / y rows arrived with the panel)
+            // w = phi'(r) on this lane's panel rows (residual and b / y rows arrived with the
+            // panel), written over the residual rows: the row loops below stay rolled (small
+            // instruction footprint) and read w back from shared memory
             const long long r0 = p * R;
-            double w[RPL];
 #pragma unroll
             for (int qq = 0; qq < RPL; ++qq) {
                 const int i = lane + 32 * qq;
-                w[qq] = (r0 + i) < P.m ? loss_prime_t<LOSS>(P.S, rsm[i], rsm[R + i]) : 0.0;
+                rsm[i] = (r0 + i) < P.m ? loss_prime_t<LOSS>(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
             sp.mark(1);
             // a free TMEM slot now?  then dot and park in ONE pass over shared memory
@@ -546,14 +550,15 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 double acc[GW];
 #pragma unroll
                 for (int c = 0; c < GW; ++c) acc[c] = 0.0;
-#pragma unroll
+#pragma unroll kRoll
                 for (int qq = 0; qq < RPL; ++qq) {
                     const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
+                    const double wq = rsm[lane + 32 * qq];
                     double v[GW];
 #pragma unroll
                     for (int c = 0; c < GW; ++c) v[c] = a[c * R];
 #pragma unroll
-                    for (int c = 0; c < GW; ++c) acc[c] = fma(v[c], w[qq], acc[c]);
+                    for (int c = 0; c < GW; ++c) acc[c] = fma(v[c], wq, acc[c]);
                     if (parked) {
                         const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
 #pragma unroll
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     tc_fence_after();
 #pragma unroll
                     for (int g0 = 0; g0 < BT; g0 += GW) {
-#pragma unroll
+#pragma unroll kRoll
                         for (int qq = 0; qq < RPL; ++qq) {
                             const double* a = pan + (size_t)g0 * R + lane + 32 * qq;
                             double v[GW];
@@ -741,7 +746,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long r0 = p * R;
             if (hd.parked) tc_fence_after();
             if (nz) {
-#pragma unroll
+#pragma unroll kRoll
                 for (int qq = 0; qq < RPL; ++qq) {
                     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
                     const long long row = r0 + lane + 32 * qq;
