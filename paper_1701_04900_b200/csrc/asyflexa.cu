@@ -563,7 +563,7 @@ static DenseKernelFn dense_kernel_for(int BT, int RPL, int NS, int loss) {
     if (BT == bt && RPL == rpl && NS == ns)                                                   \
         return loss == LOSS_LS ? dense_async_kernel<bt, rpl, ns, LOSS_LS>                     \
                                : dense_async_kernel<bt, rpl, ns, LOSS_LOGISTIC>;
-    ASY_DK(8, 8, 4) ASY_DK(16, 8, 4) ASY_DK(32, 4, 4) ASY_DK(32, 2, 8) ASY_DK(64, 2, 4) ASY_DK(128, 1, 4)
+    ASY_DK(8, 8, 4) ASY_DK(16, 8, 4) ASY_DK(32, 4, 4) ASY_DK(32, 3, 8) ASY_DK(32, 2, 8) ASY_DK(64, 2, 4) ASY_DK(128, 1, 4)
 #undef ASY_DK
     return nullptr;
 }
