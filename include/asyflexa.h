@@ -79,6 +79,7 @@ extern "C" {
 #define ASY_KERNEL_DENSE_PANEL 1 /* dense_async.cuh: G row panels of a block on G SMs, TMEM parking */
 #define ASY_KERNEL_DENSE_SLAB 2  /* dense_slab.cuh: every SM owns a row slab, per-update all-reduce */
 #define ASY_KERNEL_SPARSE 3      /* sparse_async.cuh: CSC column updates */
+#define ASY_KERNEL_DENSE_SLAB_TMEM 4 /* dense_slabt.cuh: row slabs, the tile parked in TMEM between dot and axpy */
 
 /* block schedules (S.1) [PAPER.md:253] */
 #define ASY_SCHED_CYCLIC 0  /* sequence k updates block k mod N */

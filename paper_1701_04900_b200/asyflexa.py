@@ -33,8 +33,10 @@ ASY_REG_L1, ASY_REG_EXP, ASY_REG_LOG = 0, 1, 2
 ASY_MODE_ASYNC, ASY_MODE_SYNC_JACOBI = 0, 1
 ASY_SCHED_CYCLIC, ASY_SCHED_RANDOM = 0, 1
 ASY_KERNEL_JACOBI, ASY_KERNEL_DENSE_PANEL, ASY_KERNEL_DENSE_SLAB, ASY_KERNEL_SPARSE = 0, 1, 2, 3
+ASY_KERNEL_DENSE_SLAB_TMEM = 4
 KERNEL_NAMES = {0: "jacobi (asy::dense_gemvT/gemvN)", 1: "asy::dense_async_kernel",
-                2: "asy::dense_slab_kernel", 3: "asy::sparse_async_kernel"}
+                2: "asy::dense_slab_kernel", 3: "asy::sparse_async_kernel",
+                4: "asy::dense_slabt_kernel"}
 
 _vp, _dp = C.c_void_p, C.POINTER(C.c_double)
 

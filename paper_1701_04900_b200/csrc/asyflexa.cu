@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "dense_async.cuh"
 #include "dense_slab.cuh"
+#include "dense_slabt.cuh"
 #include "sparse_async.cuh"
 #include "sync_kernels.cuh"
 
@@ -630,7 +631,6 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-
     const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
     TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * Bmax));
     TRY(dev_alloc(h, h->dpart, sizeof(double) * G * Bmax));
@@ -722,7 +722,155 @@ static SlabKernelFn slab_kernel_for(int cpw, int loss) {
     return nullptr;
 }
 
+// ---- row-slab kernel with the tile parked in TMEM (dense_slabt.cuh)
+static SlabKernelFn slabt_kernel_for(int bmax, int loss) {
+    if (loss == LOSS_LS) {
+        if (bmax == 32) return dense_slabt_kernel<32, LOSS_LS>;
+        if (bmax == 64) return dense_slabt_kernel<64, LOSS_LS>;
+        if (bmax == 128) return dense_slabt_kernel<128, LOSS_LS>;
+    } else {
+        if (bmax == 32) return dense_slabt_kernel<32, LOSS_LOGISTIC>;
+        if (bmax == 64) return dense_slabt_kernel<64, LOSS_LOGISTIC>;
+        if (bmax == 128) return dense_slabt_kernel<128, LOSS_LOGISTIC>;
+    }
+    return nullptr;
+}
+
+// Geometry of the TMEM-parking slab kernel (dense_slabt.cuh); false when its park ring
+// (TMEM + shared-memory hold slots: one whole sequence per dot warp) plus a load ring of
+// >= 4 units per dot warp does not fit on the SM, or a warp would own > kSlabTMaxG groups.
+struct SlabTGeom {
+    int grid, bmax, nsw, nhold, npark[4], hoff[4];
+    int64_t Rs;
+    size_t smem;
+};
+static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, SlabTGeom* g) {
+    const int64_t m = h->m, B = h->B;
+    if (B > 128) return false;
+    const int bmax = B <= 32 ? 32 : B <= 64 ? 64 : 128;
+    const int nsplit = bmax > 64 ? 2 : 1, CS = bmax / nsplit, SQ = 256 / CS;
+    // slabs of whole 32-row groups: ngt groups over the CTAs, ngt / grid or one more each
+    const int64_t ngt = (m + 31) / 32;
+    int64_t grid0 = h->sms;
+    if (sp->workers > 0) grid0 = std::min<int64_t>(grid0, sp->workers);
+    grid0 = std::max<int64_t>(1, std::min<int64_t>(grid0, ngt));
+    const int nrg = (int)((ngt + grid0 - 1) / grid0);  // most groups of a CTA
+    const int64_t Rs = 32 * (int64_t)nrg;
+    if ((nrg + kSlabDot - 1) / kSlabDot > kSlabTMaxG) return false;
+    int extra = 0;  // extra hold slots per warp (measurement knob)
+    if (const char* e = getenv("ASY_SLABT_EXTRA")) extra = std::max(0, atoi(e));
+    int nhold = 0;
+    for (int d = 0; d < kSlabDot; ++d) {
+        const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
+        const int hs = std::max(0, nsplit * cnt - SQ) + (cnt > 0 ? extra : 0);
+        g->hoff[d] = nhold;
+        g->npark[d] = SQ + hs;
+        nhold += hs;
+    }
+    const size_t unit = sizeof(double) * 32 * 16, hslot = sizeof(double) * 32 * CS;
+    const int64_t RsP = (Rs + 1) & ~1ll;
+    const size_t fixed = sizeof(double) * (3 * RsP + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
+                         (sizeof(SeqMeta) + sizeof(long long)) * kSlabNM +
+                         sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 2 * kSlabNDX) +
+                         sizeof(unsigned long long) * kSlabAx + sizeof(unsigned) * (kSlabDot + 1) + 256;
+    const size_t cap = 227 * 1024;
+    int nsw = kSlabTMaxStages / kSlabDot;
+    if (const char* e = getenv("ASY_SLABT_NSW")) nsw = std::max(1, std::min(nsw, atoi(e)));
+    while (nsw >= 4 && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
+    if (nsw < 4 && !getenv("ASY_SLABT_NSW")) return false;
+    if (fixed + nhold * hslot + kSlabDot * nsw * unit > cap) return false;
+    g->grid = (int)grid0;
+    g->Rs = Rs; g->bmax = bmax; g->nsw = nsw; g->nhold = nhold;
+    g->smem = fixed + nhold * hslot + kSlabDot * nsw * unit;
+    return true;
+}
+
+static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const SlabTGeom& geo, int64_t sweeps,
+                              int64_t delay, float* ms) {
+    const int64_t B = h->B;
+    delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
+    const int nsplit = geo.bmax > 64 ? 2 : 1;  // all-reduces per block update
+    const int64_t slots = next_pow2(std::max<int64_t>(64, nsplit * (2 * delay + 2)));
+    const int det = delay == 0 ? 1 : 0;
+    h->last_kernel = ASY_KERNEL_DENSE_SLAB_TMEM;
+    h->last_delay = (int)delay;
+    SlabKernelFn fn = slabt_kernel_for(geo.bmax, h->S.loss);
+    if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no TMEM slab kernel for block size %lld", (long long)B);
+    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kSlabThreads, geo.smem));
+    if (occ < 1) return h->fail(ASY_ERR_CUDA, "TMEM slab kernel does not fit on an SM");
+
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap tmap;
+    const int W = B < 16 ? (int)B : 16;  // unit box: 32 rows x 16 columns
+    cuuint64_t dims[2] = {(cuuint64_t)h->m, (cuuint64_t)h->n};
+    cuuint64_t strides[1] = {(cuuint64_t)(h->lda * sizeof(double))};
+    cuuint32_t box[2] = {32u, (cuuint32_t)W};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->A.p, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * kGaccRep * B));
+    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots * kArrivePad));
+    if (det) TRY(dev_alloc(h, h->dpart, sizeof(double) * slots * geo.grid * B));
+
+    SlabParams P{};
+    P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk;
+    P.Rs = geo.Rs; P.Rc = 32; P.nch = (int)((geo.Rs + 31) / 32); P.hold = 1;
+    P.nst = kSlabDot * geo.nsw; P.nsa = geo.nhold; P.stage_dbl = 32 * 16;
+    P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
+    P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
+    P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
+    P.K = sweeps * h->nblk; P.delay = delay; P.deterministic = det;
+    P.gacc = P_<double>(h->gacc); P.part = det ? P_<double>(h->dpart) : nullptr; P.arrive = P_<unsigned>(h->arrive);
+    P.slots = slots;
+    P.A = P_<double>(h->A); P.lda = h->lda;
+    for (int d = 0; d < 4; ++d) { P.npark[d] = geo.npark[d]; P.hoff[d] = geo.hoff[d]; }
+    const char* pf = getenv("ASY_PROF");
+    Dev prof;
+    if (pf) {
+        TRY(dev_alloc(h, prof, sizeof(unsigned long long) * geo.grid * kSlabWarps * 8));
+        CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * geo.grid * kSlabWarps * 8, h->stream));
+        P.prof = P_<unsigned long long>(prof);
+    }
+    if (getenv("ASY_SLAB_VERBOSE"))
+        fprintf(stderr, "[slabt] grid %d Rs %lld bmax %d nsw %d nhold %d npark %d/%d/%d/%d smem %zu delay %lld det %d\n",
+                geo.grid, (long long)geo.Rs, geo.bmax, geo.nsw, geo.nhold, geo.npark[0], geo.npark[1], geo.npark[2],
+                geo.npark[3], geo.smem, (long long)delay, det);
+    slab_init<<<grid_for(2 * slots * kGaccRep * B, 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    CKL();
+    void* args[] = {&tmap, &P};
+    CK(cudaEventRecord(h->ev[0], h->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(geo.grid), dim3(kSlabThreads), args, geo.smem, h->stream));
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(cudaEventSynchronize(h->ev[1]));
+    CKL();
+    CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    if (sweeps & 1) std::swap(h->x, h->xalt);
+    if (P.prof) {
+        std::vector<unsigned long long> hb((size_t)geo.grid * kSlabWarps * 8);
+        CK(cudaMemcpy(hb.data(), prof.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
+        FILE* f = fopen(pf, "wb");
+        if (f) {
+            fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
+            fclose(f);
+        }
+        dev_free(prof);
+    }
+    return ASY_OK;
+}
+
 static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay, float* ms) {
+    {
+        // the TMEM-parking form when its park ring fits (ASY_SLAB_TMEM=0: the smem / L2 form)
+        const char* te = getenv("ASY_SLAB_TMEM");
+        SlabTGeom tg;
+        if ((!te || atoi(te) != 0) && slabt_geometry(h, sp, &tg)) return dense_slabt_launch(h, sp, tg, sweeps, delay, ms);
+    }
     const int64_t m = h->m, B = h->B;
     const int cpw = B <= 32 ? 8 : B <= 64 ? 16 : 32;
     const int BMAX = kSlabDot * cpw;
@@ -784,7 +932,9 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     // delay: the L2 must still hold a block between its dot pass and its re-load
     if (!hold) {
         const double blk_bytes = 8.0 * (double)m * (double)B;
-        const int64_t l2cap = std::max<int64_t>(1, (int64_t)(40e6 / blk_bytes));
+        const char* l2e = getenv("ASY_SLAB_L2MB");  // measurement override of the L2 budget
+        const double l2b = (l2e ? atof(l2e) : 40.0) * 1e6;
+        const int64_t l2cap = std::max<int64_t>(1, (int64_t)(l2b / blk_bytes));
         delay = std::min(delay, l2cap);
     }
     delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
@@ -811,8 +961,8 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
 
-    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * B));
-    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * kGaccRep * B));
+    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots * kArrivePad));
     if (det) TRY(dev_alloc(h, h->dpart, sizeof(double) * slots * grid * B));
 
     SlabParams P{};
@@ -834,7 +984,7 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     if (getenv("ASY_SLAB_VERBOSE"))
         fprintf(stderr, "[slab] grid %d Rs %lld Rc %d nch %d hold %d nst %d nsa %d smem %zu delay %lld slots %lld det %d\n",
                 grid, (long long)Rs, Rc, nch, hold, nst, nsa, smem, (long long)delay, (long long)slots, det);
-    slab_init<<<grid_for(2 * slots * B, 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    slab_init<<<grid_for(2 * slots * kGaccRep * B, 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
     void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));

@@ -65,6 +65,11 @@ constexpr int kSlabWarps = kSlabSeq0 + kSlabSeq;
 constexpr int kSlabThreads = 32 * kSlabWarps;
 constexpr int kSlabNP = kSlabSeq;   // partial ring: slot k mod 6 <-> sequence warp k mod 6
 constexpr int kSlabNDX = kSlabSeq;  // dx ring
+// All-reduce layout: CTA c adds its partial into replica c mod kGaccRep of the slot (148 CTAs
+// adding into one copy serialise ~150 fp64 atomics per address on a few L2 slices); readers
+// sum the replicas.  Arrival counters sit one per 128-byte line (hundreds of warps poll them).
+constexpr int kGaccRep = 8;
+constexpr int kArrivePad = 32;
 constexpr int kSlabMaxStages = 24;
 constexpr int kSlabPad = 32;        // zero doubles after each stage (reads past the last column)
 
@@ -89,18 +94,23 @@ struct SlabParams {
     int64_t K;         // sequences in this launch
     int64_t delay;     // bounded delay (effective)
     int deterministic;
-    double* gacc;      // [S][2][B]
+    double* gacc;      // [S][2][kGaccRep][B]
     double* part;      // [S][grid][B]   (deterministic)
-    unsigned* arrive;  // [S] monotonic
+    unsigned* arrive;  // [S * kArrivePad] monotonic (slot s at s * kArrivePad)
     int64_t slots;     // S, power of two, >= 2*delay + 2
     unsigned long long* prof;  // optional [grid][kSlabWarps][8] clock64 segment sums
+    // TMEM-parking form only (dense_slabt.cuh)
+    const double* A;   // column-major, for the 1-D bulk copies of a slab's ragged last row group
+    int64_t lda;
+    int npark[4];      // park ring per dot warp d: TMEM slots (256 / BMAX) + its smem hold slots
+    int hoff[4];       // first smem hold slot of dot warp d
 };
 
 __global__ void slab_init(SlabParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t s = tid; s < P.slots; s += nth) P.arrive[s] = 0u;
-    for (int64_t i = tid; i < 2 * P.slots * P.B; i += nth) P.gacc[i] = 0.0;
+    for (int64_t s = tid; s < P.slots; s += nth) P.arrive[s * kArrivePad] = 0u;
+    for (int64_t i = tid; i < 2 * P.slots * kGaccRep * P.B; i += nth) P.gacc[i] = 0.0;
 }
 
 __device__ __forceinline__ void slab_tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
@@ -214,6 +224,170 @@ struct RingPos {
     }
 };
 
+// The schedule walk of one CTA's producer (S.1): block b of sequence k, the index of
+// the previous update of b (D4, via the inverse permutation: schedule_prev) and the
+// sequence's guard need = max(k - delay, kprev + 1).  Sequences are visited in order.
+struct SlabSchedule {
+    PermKeys pk, pkp;
+    int half;
+    int64_t e, i;  // local epoch, position in it
+    int kmod;      // k mod grid
+    __device__ void init(int64_t N) {
+        half = perm_half_bits(N);
+        e = 0; i = 0; kmod = 0;
+    }
+    __device__ SeqMeta next(const SlabParams& P, int64_t k) {
+        const int64_t N = P.nblk;
+        if (i == 0 && P.sched == SCHED_RANDOM) {
+            pk = perm_keys(P.seed, P.epoch0 + e);
+            if (P.epoch0 + e > 0) pkp = perm_keys(P.seed, P.epoch0 + e - 1);
+        }
+        int64_t b = i, kprev = -1;
+        if (P.sched == SCHED_RANDOM) {
+            uint64_t v = (uint64_t)i;
+            do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
+            b = (int64_t)v;
+        }
+        if (P.epoch0 + e > 0) {
+            int64_t pos = b;
+            if (P.sched == SCHED_RANDOM) {
+                uint64_t v = (uint64_t)b;
+                do { v = feistel_inv(v, half, pkp); } while (v >= (uint64_t)N);
+                pos = (int64_t)v;
+            }
+            kprev = (e - 1) * N + pos;  // local index (negative: an earlier launch)
+        }
+        SeqMeta md;
+        md.need = k - P.delay;
+        if (kprev + 1 > md.need) md.need = kprev + 1;
+        md.b = (int32_t)b;
+        md.flags = (int32_t)(e & 1) | (kmod == (int)blockIdx.x ? 2 : 0);
+        if (++i == N) { i = 0; ++e; }
+        if (++kmod == (int)gridDim.x) kmod = 0;
+        return md;
+    }
+};
+
+// Sequence warp q (of kSlabSeq): for its sequences k = q, q + 6, ... sums the CTA's
+// kSlabDot partials (fixed order), publishes them into the grid-wide accumulator,
+// waits for all CTAs, solves the block subproblem (Eq. 2 closed form) + (S.4) and
+// hands dx_b to the axpy warps; CTA k mod grid stores x_b.  Shared by both slab kernels.
+template <int BMAX, int NSPLIT = 1>
+__device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, int lane, const double* pring,
+                                                   double* dxring, const SeqMeta* meta, uint64_t* pfull,
+                                                   uint64_t* pempty, uint64_t* dxfull, uint64_t* dxempty,
+                                                   SlabProf& sp) {
+    const int64_t K = P.K;
+    const int B = (int)P.B;
+    const int64_t S = P.slots;
+    int lgS = 0;
+    while (((int64_t)1 << lgS) < S) ++lgS;
+    const unsigned grid = gridDim.x;
+    constexpr int CS = BMAX / NSPLIT;  // columns of a sub-sequence
+    constexpr int PER = CS / 32;        // block columns per lane
+    // this warp's sub-sequences s = q + 6 t (s = k * NSPLIT + h: columns [h CS, h CS + CS) of
+    // sequence k's block) use ring slot q, phase t & 1
+    uint32_t ph = 0;
+    for (int64_t s = q; s < K * NSPLIT; s += kSlabSeq, ph ^= 1u) {
+        const int64_t k = s / NSPLIT;
+        const int h = (int)(s - k * NSPLIT);
+        // the CTA's partial (the dot warps' arrivals also publish the sequence's metadata)
+        mbar_wait(&pfull[q], ph);
+        sp.mark(1);
+        const SeqMeta md = meta[k & (kSlabNM - 1)];
+        const int64_t c0 = (int64_t)md.b * P.B + h * CS;
+        const int nc = (int)max((int64_t)0, min(min((int64_t)CS, P.B - h * CS), P.n - c0));
+        const int64_t slot = s & (S - 1), use = s >> lgS;
+        const int half = (int)(use & 1);
+        const double* xr = (md.flags & 1) ? P.x1 : P.x0;
+        double* xw = (md.flags & 1) ? P.x0 : P.x1;
+        double pv[PER], tpre[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int cc = lane + 32 * e;
+            const double* pw = pring + (size_t)q * kSlabDot * CS + cc;
+            pv[e] = ((pw[0] + pw[CS]) + pw[2 * CS]) + pw[3 * CS];  // fixed order
+            tpre[e] = cc < nc ? P.tau[c0 + cc] : 1.0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[q]);
+        // publish
+        const int rep = (int)(blockIdx.x % kGaccRep);
+        double* gk = P.gacc + (slot * 2 + half) * kGaccRep * P.B;  // replica 0 of the slot half
+        double* gmine = gk + rep * P.B;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int cc = lane + 32 * e;
+            if (cc < nc) {
+                if (P.deterministic) P.part[(slot * grid + blockIdx.x) * P.B + cc] = pv[e];
+                else atomicAdd(&gmine[cc], pv[e]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) red_release_gpu_u32(&P.arrive[slot * kArrivePad], 1u);
+        sp.mark(2);
+        // all CTAs' partials of sub-sequence s
+        if (lane == 0) spin_until_ge_relaxed_u32(&P.arrive[slot * kArrivePad], (unsigned)(use + 1) * grid);
+        __syncwarp();
+        sp.mark(3);
+        double g[PER], y[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int cc = lane + 32 * e;
+            g[e] = 0.0;
+            y[e] = 0.0;
+            if (cc < nc) {
+                if (P.deterministic) {
+                    for (unsigned tt = 0; tt < grid; ++tt)
+                        g[e] += ld_relaxed_f64(&P.part[(slot * grid + tt) * P.B + cc]);
+                } else {
+                    double gr[kGaccRep];
+#pragma unroll
+                    for (int r = 0; r < kGaccRep; ++r) gr[r] = ld_relaxed_f64(&gk[r * P.B + cc]);
+#pragma unroll
+                    for (int r = 0; r < kGaccRep; ++r) g[e] += gr[r];
+                }
+                y[e] = ld_relaxed_f64(&xr[c0 + cc]);
+            }
+        }
+        if (!P.deterministic) {
+            double* gn = P.gacc + ((slot * 2 + (half ^ 1)) * kGaccRep + rep) * P.B;  // my replica
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int cc = lane + 32 * e;
+                if (cc < B && cc < CS) gn[cc] = 0.0;
+            }
+        }
+        // block subproblem (Eq. 2, closed form) and (S.4)
+        double xn[PER], dd[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int cc = lane + 32 * e;
+            xn[e] = y[e];
+            dd[e] = 0.0;
+            if (cc < nc) {
+                const double xh = best_response(P.S, g[e], y[e], tpre[e], c0 + cc);
+                xn[e] = y[e] + P.gamma * (xh - y[e]);
+                dd[e] = xn[e] - y[e];
+            }
+        }
+        if (s >= kSlabNDX) mbar_wait(&dxempty[q], ph ^ 1u);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) dxring[q * CS + lane + 32 * e] = dd[e];
+        if (md.flags & 2) {
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int cc = lane + 32 * e;
+                if (cc < nc) xw[c0 + cc] = xn[e];
+            }
+            fence_acq_rel_gpu();  // x_b visible before this CTA's later arrivals (D4 readers)
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dxfull[q]);
+        sp.mark(4);
+    }
+}
+
 // CPW = 8, 16 or 32: blocks of up to BMAX = 4 * CPW columns.  LOSS: LOSS_LS / LOSS_LOGISTIC
 // (compile-time: keeps the instruction footprint of the hot loops small).
 template <int CPW, int LOSS>
@@ -292,46 +466,22 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         // ---------------------------------------------------------------- dot producer (+ schedule)
         if (lane == 0) {
             const uint64_t pol = P.hold ? policy_evict_first() : policy_evict_last();
-            const int half = perm_half_bits(N);
-            PermKeys pk{}, pkp{};
-            int64_t e = 0, i = 0;  // local epoch, position in it
-            int kmod = 0;          // k mod grid
+            SlabSchedule sch;
+            sch.init(N);
             // chunk c goes to sub-ring c mod 4 at position (c / 4) mod nsw: the four sub-rings
             // advance together, one position per group of four chunks
             RingPos gp;
             gp.init(nsw);
             int64_t c = 0;
             for (int64_t k = 0; k < K; ++k) {
-                if (i == 0 && P.sched == SCHED_RANDOM) {
-                    pk = perm_keys(P.seed, P.epoch0 + e);
-                    if (P.epoch0 + e > 0) pkp = perm_keys(P.seed, P.epoch0 + e - 1);
-                }
-                int64_t b = i, kprev = -1;
-                if (P.sched == SCHED_RANDOM) {
-                    uint64_t v = (uint64_t)i;
-                    do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
-                    b = (int64_t)v;
-                }
-                if (P.epoch0 + e > 0) {
-                    int64_t pos = b;
-                    if (P.sched == SCHED_RANDOM) {
-                        uint64_t v = (uint64_t)b;
-                        do { v = feistel_inv(v, half, pkp); } while (v >= (uint64_t)N);
-                        pos = (int64_t)v;
-                    }
-                    kprev = (e - 1) * N + pos;  // local index (negative: an earlier launch)
-                }
-                int64_t need = k - P.delay;
-                if (kprev + 1 > need) need = kprev + 1;
+                const SeqMeta mk = sch.next(P, k);
+                const int64_t b = mk.b;
                 // the metadata slot of sequence k - NM is free once its axpy is done
                 if (k >= kSlabNM) {
                     for (int a = 0; a < kSlabAx; ++a)
                         while (ld_acquire_cta_u64(&progress[a]) < (unsigned long long)(k - kSlabNM + 1)) __nanosleep(32);
                 }
-                SeqMeta& md = meta[k & (kSlabNM - 1)];
-                md.need = need;
-                md.b = (int32_t)b;
-                md.flags = (int32_t)(e & 1) | (kmod == (int)blockIdx.x ? 2 : 0);
+                meta[k & (kSlabNM - 1)] = mk;
                 for (int ch = 0; ch < nch; ++ch, ++c) {
                     const int w = (int)(c & (kSlabDot - 1));
                     const int st = w * nsw + gp.i;
@@ -342,8 +492,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                                 pol);
                     if (w == kSlabDot - 1) gp.next();
                 }
-                if (++i == N) { i = 0; ++e; }
-                if (++kmod == (int)gridDim.x) kmod = 0;
             }
         }
         sp.mark(0);
@@ -500,105 +648,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             sp.mark(4);
         }
     } else {
-        // ---------------------------------------------------------------- sequence warps
-        const int q = warp - kSlabSeq0;
-        const int64_t S = P.slots;
-        int lgS = 0;
-        while (((int64_t)1 << lgS) < S) ++lgS;
-        const unsigned grid = gridDim.x;
-        constexpr int PER = BMAX / 32;  // block columns per lane
-        // this warp's sequences k = q + 6 t use ring slot q, phase t & 1
-        uint32_t ph = 0;
-        for (int64_t k = q; k < K; k += kSlabSeq, ph ^= 1u) {
-            // the CTA's partial (the dot warps' arrivals also publish the sequence's metadata)
-            mbar_wait(&pfull[q], ph);
-            sp.mark(1);
-            const SeqMeta md = meta[k & (kSlabNM - 1)];
-            const int64_t c0 = (int64_t)md.b * P.B;
-            const int nc = (int)min(P.B, P.n - c0);
-            const int64_t slot = k & (S - 1), use = k >> lgS;
-            const int half = (int)(use & 1);
-            const double* xr = (md.flags & 1) ? P.x1 : P.x0;
-            double* xw = (md.flags & 1) ? P.x0 : P.x1;
-            double pv[PER], tpre[PER];
-#pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int cc = lane + 32 * e;
-                const double* pw = pring + (size_t)q * kSlabDot * BMAX + cc;
-                pv[e] = ((pw[0] + pw[BMAX]) + pw[2 * BMAX]) + pw[3 * BMAX];  // fixed order
-                tpre[e] = cc < nc ? P.tau[c0 + cc] : 1.0;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pempty[q]);
-            // publish
-            double* gk = P.gacc + (slot * 2 + half) * P.B;
-#pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int cc = lane + 32 * e;
-                if (cc < nc) {
-                    if (P.deterministic) P.part[(slot * grid + blockIdx.x) * P.B + cc] = pv[e];
-                    else atomicAdd(&gk[cc], pv[e]);
-                }
-            }
-            __syncwarp();
-            if (lane == 0) red_release_gpu_u32(&P.arrive[slot], 1u);
-            sp.mark(2);
-            // all CTAs' partials of sequence k
-            if (lane == 0) spin_until_ge_relaxed_u32(&P.arrive[slot], (unsigned)(use + 1) * grid);
-            __syncwarp();
-            sp.mark(3);
-            double g[PER], y[PER];
-#pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int cc = lane + 32 * e;
-                g[e] = 0.0;
-                y[e] = 0.0;
-                if (cc < nc) {
-                    if (P.deterministic) {
-                        for (unsigned tt = 0; tt < grid; ++tt)
-                            g[e] += ld_relaxed_f64(&P.part[(slot * grid + tt) * P.B + cc]);
-                    } else {
-                        g[e] = ld_relaxed_f64(&gk[cc]);
-                    }
-                    y[e] = ld_relaxed_f64(&xr[c0 + cc]);
-                }
-            }
-            if (!P.deterministic) {
-                double* gn = P.gacc + (slot * 2 + (half ^ 1)) * P.B;
-#pragma unroll
-                for (int e = 0; e < PER; ++e) {
-                    const int cc = lane + 32 * e;
-                    if (cc < B) gn[cc] = 0.0;
-                }
-            }
-            // block subproblem (Eq. 2, closed form) and (S.4)
-            double xn[PER], dd[PER];
-#pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int cc = lane + 32 * e;
-                xn[e] = y[e];
-                dd[e] = 0.0;
-                if (cc < nc) {
-                    const double xh = best_response(P.S, g[e], y[e], tpre[e], c0 + cc);
-                    xn[e] = y[e] + P.gamma * (xh - y[e]);
-                    dd[e] = xn[e] - y[e];
-                }
-            }
-            if (k >= kSlabNDX) mbar_wait(&dxempty[q], ph ^ 1u);
-#pragma unroll
-            for (int e = 0; e < PER; ++e) dxring[q * BMAX + lane + 32 * e] = dd[e];
-            if (md.flags & 2) {
-#pragma unroll
-                for (int e = 0; e < PER; ++e) {
-                    const int cc = lane + 32 * e;
-                    if (cc < nc) xw[c0 + cc] = xn[e];
-                }
-                fence_acq_rel_gpu();  // x_b visible before this CTA's later arrivals (D4 readers)
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&dxfull[q]);
-            sp.mark(4);
-        }
+        slab_sequence_warp<BMAX>(P, warp - kSlabSeq0, lane, pring, dxring, meta, pfull, pempty, dxfull, dxempty, sp);
     }
     sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * kSlabWarps + warp) * 8 : nullptr, lane);
     __syncthreads();

@@ -1,0 +1,417 @@
+// dense_slabt.cuh -- row-slab asynchronous block-update kernel with the tile parked in TMEM.
+//
+// Same method as dense_slab.cuh (Algorithm 1 [PAPER.md:246-260]; one persistent CTA per
+// SM owns rows [row0, row0 + rows) of A, r and b / y; every block update is a grid-wide
+// all-reduce of per-slab partials; bounded delay D1 [PAPER.md:224] and own-block
+// freshness D4 [PAPER.md:233] enforced per CTA), organised so that HBM streams while
+// the all-reduces are in flight:
+//
+//   * the slab is cut into 32-row groups g (the last one ragged).  Dot warp d and axpy
+//     warp d own the groups g = d (mod 4) for the whole launch: they share one TMEM lane
+//     quarter (warp id mod 4), lane = row, and the axpy warp is the only writer of those
+//     rows of the residual slab, the dot warp their only reader besides it;
+//   * a block's columns are processed as NSPLIT "sub-sequences" of CS = BMAX / NSPLIT
+//     columns (CS = 64 for blocks of 65-128 columns, else the whole block): each has its
+//     own all-reduce, so the all-reduce of columns [0, 64) overlaps the loads of columns
+//     [64, 128).  The gradient of all sub-sequences is taken from ONE residual snapshot
+//     (w = phi'(r) is computed once per sequence and kept in registers), and the axpy of
+//     the first sub-sequences goes to a pending buffer (delta) that is added to r together
+//     with the last one -- every residual row always holds whole block updates (reading
+//     R8 of DESIGN.md is unchanged);
+//   * slabs are whole 32-row groups (CTAs own ngt / grid or one more), so every unit is one
+//     2-D TMA box of 32 rows x 16 columns (4 KB); lanes 0-3 of warp 1 issue the four dot
+//     warps' unit streams in lockstep into per-warp rings of nsw stages.  Units are taken
+//     column block by column block across a warp's groups, so one butterfly reduction
+//     covers all its rows;
+//   * in the same pass over shared memory each unit is parked in its group's park slot
+//     (TMEM, tcgen05.st 32x32b; shared-memory hold slots for what does not fit in the
+//     256 KB of TMEM) and its stage is refilled immediately;
+//   * the axpy warp applies r_g += A[g, cols] dx from the park slot (tcgen05.ld / lds) and
+//     frees it.
+// Warp 0 only evaluates the schedule (metadata ring, ready flags).  A park slot is waited
+// for before the dot pass of a sub-sequence; the ring holds one whole sequence per warp,
+// so the slot was used by the previous sequence's same sub-sequence, whose dx only needs
+// partials every CTA has already published: no deadlock.
+// delay == 0: sequential and bit-reproducible, as in dense_slab.cuh.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "dense_async.cuh"
+#include "dense_slab.cuh"
+
+namespace asy {
+
+constexpr int kSlabTMaxStages = 64;  // 4 dot warps x nsw
+constexpr int kSlabTMaxG = 4;        // row groups per warp per sequence (slabs <= 512 rows)
+
+template <int BMAX, int LOSS>
+__global__ void __launch_bounds__(kSlabThreads, 1)
+    dense_slabt_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams P) {
+    constexpr int NSPLIT = BMAX > 64 ? 2 : 1;  // sub-sequences per block update
+    constexpr int CS = BMAX / NSPLIT;          // columns of a sub-sequence
+    constexpr int SQ = 256 / CS;               // TMEM park slots per lane quarter (2*CS b32 columns)
+    constexpr int UNIT = 32 * 16;              // doubles per unit stage (4 KB)
+    constexpr int HSLOT = 32 * CS;             // doubles per smem hold slot
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int nsw = P.nst / kSlabDot;
+    const int64_t RsP = (P.Rs + 1) & ~(int64_t)1;
+    double* dstage = reinterpret_cast<double*>(smem_raw);            // nst * UNIT
+    double* hold = dstage + (size_t)P.nst * UNIT;                     // nsa * HSLOT
+    double* rs = hold + (size_t)P.nsa * HSLOT;                        // Rs   residual slab
+    double* auxs = rs + RsP;                                          // Rs   b / y slab
+    double* delta = auxs + RsP;                                       // Rs   pending sub-sequence axpy
+    double* pring = delta + RsP;                                      // NP * kSlabDot * CS
+    double* dxring = pring + kSlabNP * kSlabDot * CS;                 // NDX * CS
+    SeqMeta* meta = reinterpret_cast<SeqMeta*>(dxring + kSlabNDX * CS);  // NM
+    long long* meta_k = reinterpret_cast<long long*>(meta + kSlabNM);    // NM ready flags
+    uint64_t* bars = reinterpret_cast<uint64_t*>(meta_k + kSlabNM);
+    uint64_t* dfull = bars;                       // nst
+    uint64_t* dempty = dfull + kSlabTMaxStages;   // nst
+    uint64_t* pfull = dempty + kSlabTMaxStages;   // NP
+    uint64_t* pempty = pfull + kSlabNP;           // NP
+    uint64_t* dxfull = pempty + kSlabNP;          // NDX
+    uint64_t* dxempty = dxfull + kSlabNDX;        // NDX
+    unsigned long long* progress = reinterpret_cast<unsigned long long*>(dxempty + kSlabNDX);  // kSlabAx
+    unsigned* parked_done = reinterpret_cast<unsigned*>(progress + kSlabAx);                   // kSlabDot
+    uint32_t* tmem_base_s = parked_done + kSlabDot;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // slabs are whole 32-row groups: CTA s owns groups [gs, gs + ng), ng = base or base + 1; only
+    // the matrix's last group can be short (the TMA zero-fills its rows >= m)
+    const int64_t ngt = (P.m + 31) / 32, gbase = ngt / gridDim.x, gextra = ngt % gridDim.x;
+    const int nrg = (int)(gbase + ((int64_t)blockIdx.x < gextra ? 1 : 0));         // my row groups
+    const int64_t row0 = 32 * ((int64_t)blockIdx.x * gbase + min((int64_t)blockIdx.x, gextra));
+    const int rows = (int)max((int64_t)0, min((int64_t)32 * nrg, P.m - row0));     // this CTA's slab rows
+    const int64_t K = P.K, N = P.nblk;
+    const int B = (int)P.B;
+
+    // ---- init
+    for (int64_t i = threadIdx.x; i < (int64_t)P.nst * UNIT + (int64_t)P.nsa * HSLOT; i += blockDim.x) dstage[i] = 0.0;
+    for (int i = threadIdx.x; i < kSlabNP * kSlabDot * CS + kSlabNDX * CS; i += blockDim.x) pring[i] = 0.0;
+    for (int i = threadIdx.x; i < P.Rs; i += blockDim.x) {
+        rs[i] = i < rows ? P.r[row0 + i] : 0.0;
+        auxs[i] = i < rows ? P.aux[row0 + i] : 0.0;
+        delta[i] = 0.0;
+    }
+    for (int i = threadIdx.x; i < kSlabNM; i += blockDim.x) meta_k[i] = -1;
+    if (warp == 0) tmem_alloc_512(tmem_base_s);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P.nst; ++s) {
+            mbar_init(&dfull[s], 1);
+            mbar_init(&dempty[s], 1);
+        }
+        for (int s = 0; s < kSlabNP; ++s) {
+            mbar_init(&pfull[s], kSlabDot);
+            mbar_init(&pempty[s], 1);
+        }
+        for (int s = 0; s < kSlabNDX; ++s) {
+            mbar_init(&dxfull[s], 1);
+            mbar_init(&dxempty[s], kSlabAx);
+        }
+        for (int a = 0; a < kSlabAx; ++a) progress[a] = 0ull;
+        for (int d = 0; d < kSlabDot; ++d) parked_done[d] = 0u;
+        mbar_fence_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_s;
+    // zero the TMEM (park slots are written only over the columns of the block's column
+    // blocks; the axpy reads whole slots, so the rest must hold finite values)
+    if (warp >= kSlabDot0 && warp < kSlabAx0) {
+        const uint32_t tq = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+        double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c = 0; c < 512; c += 16) tmem_st8(tq + (uint32_t)c, z);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    SlabProf sp;
+    sp.start();
+    if (warp == 0) {
+        // ---------------------------------------------------------------- schedule (S.1)
+        if (lane == 0) {
+            SlabSchedule sch;
+            sch.init(N);
+            for (int64_t k = 0; k < K; ++k) {
+                const SeqMeta mk = sch.next(P, k);
+                // the metadata slot of sequence k - NM is free once its axpy is done
+                if (k >= kSlabNM) {
+                    for (int a = 0; a < kSlabAx; ++a)
+                        while (ld_acquire_cta_u64(&progress[a]) < (unsigned long long)(k - kSlabNM + 1)) __nanosleep(64);
+                }
+                meta[k & (kSlabNM - 1)] = mk;
+                asm volatile("st.release.cta.shared.b64 [%0], %1;" ::"r"(smem_u32(&meta_k[k & (kSlabNM - 1)])),
+                             "l"((long long)k)
+                             : "memory");
+            }
+        }
+        sp.mark(0);
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- loads (all four dot rings)
+        // Lane d < 4 owns dot warp d's unit stream: for k, h < NSPLIT, 16-column block cb,
+        // i < cnt_d: rows of group d + 4 i, columns [b B + h CS + 16 cb, +16).  The four lanes
+        // run in lockstep and issue in the same instruction whenever their ring has a free
+        // stage (a thread sustains only ~1 bulk copy per ~450 ns, tools/mb_tma.cu), and no
+        // ring waits for another (a dot warp waiting for a park slot holds only its stages).
+        const int W = B < 16 ? B : 16;  // unit columns loaded
+        const uint32_t box_bytes = 32u * (uint32_t)W * 8u;
+        const uint64_t pol = policy_evict_first();
+        const int d = lane;
+        const int cnt = (lane < kSlabDot && nrg > d) ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
+        int ist = 0, first = 1, ih = 0, icb = 0, ii = 0;
+        uint32_t iph = 0;
+        int64_t ik = cnt > 0 ? 0 : K, icol0 = 0, icached = -1;
+        for (;;) {
+            const bool live = ik < K;
+            if (!__any_sync(0xffffffffu, live)) break;
+            bool ok = false;
+            const int st = d * nsw + ist;
+            if (live) {
+                ok = first || mbar_test(&dempty[st], iph ^ 1u);
+                if (ok && icached != ik) {
+                    long long v;
+                    asm volatile("ld.acquire.cta.shared.b64 %0, [%1];"
+                                 : "=l"(v)
+                                 : "r"(smem_u32(&meta_k[ik & (kSlabNM - 1)]))
+                                 : "memory");
+                    ok = v == ik;
+                    if (ok) {
+                        icol0 = (int64_t)meta[ik & (kSlabNM - 1)].b * P.B;
+                        icached = ik;
+                    }
+                }
+            }
+            if (ok) {
+                const int g = d + kSlabDot * ii;
+                mbar_arrive_expect_tx(&dfull[st], box_bytes);
+                slab_tma_2d(dstage + (size_t)st * UNIT, &tmap, (int)(row0 + 32 * g), (int)(icol0 + ih * CS + icb * 16),
+                            &dfull[st], pol);
+                if (++ist == nsw) { ist = 0; iph ^= 1u; first = 0; }
+                if (++ii == cnt) {
+                    ii = 0;
+                    const int bh = min(CS, B - ih * CS);
+                    if (++icb == (bh <= 0 ? 0 : (bh + 15) >> 4)) {
+                        icb = 0;
+                        if (++ih == NSPLIT) { ih = 0; ++ik; }
+                    }
+                }
+            }
+            if (!__any_sync(0xffffffffu, ok)) __nanosleep(32);
+        }
+        sp.mark(0);
+    } else if (warp < kSlabAx0) {
+        // ---------------------------------------------------------------- dot warps
+        const int d = warp - kSlabDot0;
+        const uint32_t tq = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+        const int np = P.npark[d];
+        double* myhold = hold + (size_t)P.hoff[d] * HSLOT;
+        uint64_t* myfull = dfull + d * nsw;
+        uint64_t* myempty = dempty + d * nsw;
+        const double* mystage = dstage + (size_t)d * nsw * UNIT;
+        const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;  // my row groups
+        // column blocks of sub-sequence h (blocks narrower than BMAX skip the empty ones)
+        auto ncb_of = [&](int h) {
+            const int bh = min(CS, B - h * CS);
+            return bh <= 0 ? 0 : (bh + 15) >> 4;
+        };
+        RingPos pp;
+        pp.init(kSlabNP);
+        RingPos cr;         // consumed units: stage, phase
+        cr.init(nsw);
+        unsigned used = 0;  // park slots taken
+        int pslot = 0;      // used mod np
+        for (int64_t k = 0; k < K; ++k) {
+            double w[kSlabTMaxG];
+            if (cnt > 0) {
+                // D1 / D4 guards: axpy(k - delay - 1) and axpy(kprev) applied to my rows
+                if (lane == 0) {
+                    long long v;
+                    for (;;) {
+                        asm volatile("ld.acquire.cta.shared.b64 %0, [%1];"
+                                     : "=l"(v)
+                                     : "r"(smem_u32(&meta_k[k & (kSlabNM - 1)]))
+                                     : "memory");
+                        if (v == k) break;
+                        __nanosleep(32);
+                    }
+                }
+                __syncwarp();
+                const int64_t need = meta[k & (kSlabNM - 1)].need;
+                if (need > 0)
+                    while (ld_acquire_cta_u64(&progress[d]) < (unsigned long long)need) __nanosleep(20);
+                sp.mark(1);
+                // one residual snapshot for the whole block update
+#pragma unroll
+                for (int i = 0; i < kSlabTMaxG; ++i) {
+                    const int srow = 32 * (d + kSlabDot * i) + lane;
+                    w[i] = (i < cnt && srow < rows) ? loss_prime_t<LOSS>(P.S, rs[srow], auxs[srow]) : 0.0;
+                }
+            }
+#pragma unroll 1
+            for (int h = 0; h < NSPLIT; ++h) {
+                const int ncb = cnt > 0 ? ncb_of(h) : 0;
+                // partial ring slot of sub-sequence s = k * NSPLIT + h
+                if (k * NSPLIT + h >= kSlabNP) mbar_wait(&pempty[pp.i], pp.ph ^ 1u);
+                double* pdst = pring + (size_t)(pp.i * kSlabDot + d) * CS;
+                if (ncb > 0) {
+                    // park slots used..used+cnt-1: free once the axpy consumed the slots parked np ago
+                    if (used + (unsigned)cnt > (unsigned)np) {
+                        const unsigned want = used + (unsigned)cnt - (unsigned)np;
+                        while (ld_acquire_cta_u32(&parked_done[d]) < want) __nanosleep(20);
+                    }
+                    tc_fence_after();
+                    sp.mark(5);
+#pragma unroll 1
+                    for (int cb = 0; cb < ncb; ++cb) {
+                        double acc[16];
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+#pragma unroll 1
+                        for (int i = 0; i < cnt; ++i) {
+                            {
+                                const double wi = i == 0 ? w[0] : i == 1 ? w[1] : i == 2 ? w[2] : w[3];
+                                const int st = cr.i;
+                                sp.mark(3);
+                                mbar_wait(&myfull[st], cr.ph);
+                                sp.mark(6);
+                                const double* a = mystage + (size_t)st * UNIT + lane;
+                                double v[16];
+#pragma unroll
+                                for (int c = 0; c < 16; ++c) v[c] = a[c * 32];
+#pragma unroll
+                                for (int c = 0; c < 16; ++c) acc[c] = fma(v[c], wi, acc[c]);
+                                int ps = pslot + i;
+                                if (ps >= np) ps -= np;
+                                if (ps < SQ) {
+                                    const uint32_t t = tq + (uint32_t)(ps * 2 * CS + 2 * 16 * cb);
+                                    tmem_st8(t, v);
+                                    tmem_st8(t + 16, v + 8);
+                                } else {
+                                    double* hp = myhold + (size_t)(ps - SQ) * HSLOT + cb * 16 * 32 + lane;
+#pragma unroll
+                                    for (int c = 0; c < 16; ++c) hp[c * 32] = v[c];
+                                }
+                                sp.mark(2);
+                                __syncwarp();       // every lane's reads of the stage are done
+                                if (lane == 0) mbar_arrive(&myempty[st]);
+                                cr.next();
+                            }
+                        }
+                        sp.mark(3);
+                        const double colsum = slab_reduce16(acc, lane);
+                        if (lane < 16) pdst[cb * 16 + lane] = colsum;
+                        sp.mark(7);
+                    }
+                    used += (unsigned)cnt;
+                    pslot += cnt;
+                    if (pslot >= np) pslot -= np;
+                    tmem_wait_st();
+                    tc_fence_before();
+                    sp.mark(0);
+                } else {
+                    // no rows (or no columns in this sub-sequence): a zero partial
+                    for (int c = lane; c < CS; c += 32) pdst[c] = 0.0;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pfull[pp.i]);
+                pp.next();
+                sp.mark(4);
+            }
+        }
+    } else if (warp < kSlabSeq0) {
+        // ---------------------------------------------------------------- axpy warps
+        const int a = warp - kSlabAx0;  // same TMEM lane quarter and rows as dot warp a
+        const uint32_t tq = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+        const int np = P.npark[a];
+        const double* myhold = hold + (size_t)P.hoff[a] * HSLOT;
+        const int cnt = nrg > a ? (nrg - a + kSlabDot - 1) / kSlabDot : 0;
+        RingPos xp;
+        xp.init(kSlabNDX);
+        unsigned fin = 0;
+        int pslot = 0;
+        for (int64_t s = 0; s < K * NSPLIT; ++s) {
+            const int64_t k = s / NSPLIT;
+            const int h = (int)(s - k * NSPLIT);
+            const int bh = min(CS, B - h * CS);
+            mbar_wait(&dxfull[xp.i], xp.ph);
+            sp.mark(1);
+            const double* dxv = dxring + xp.i * CS;
+            if (bh > 0) {
+                for (int i = 0; i < cnt; ++i) {
+                    const int srow = 32 * (a + kSlabDot * i) + lane;
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                    int ps = pslot + i;
+                    if (ps >= np) ps -= np;
+                    if (ps < SQ) {
+                        tc_fence_after();
+                        const uint32_t t = tq + (uint32_t)(ps * 2 * CS);
+#pragma unroll
+                        for (int c32 = 0; c32 < CS; c32 += 16) {
+                            uint32_t uu[32];
+#pragma unroll
+                            for (int s8 = 0; s8 < 2; ++s8) tmem_ld8(t + (uint32_t)(2 * (c32 + 8 * s8)), uu + 16 * s8);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int c = 0; c < 16; c += 2) {
+                                const double2 d2 = *reinterpret_cast<const double2*>(dxv + c32 + c);
+                                s4[c & 3] = fma(u2d(uu[2 * c], uu[2 * c + 1]), d2.x, s4[c & 3]);
+                                s4[(c + 1) & 3] = fma(u2d(uu[2 * c + 2], uu[2 * c + 3]), d2.y, s4[(c + 1) & 3]);
+                            }
+                        }
+                        tc_fence_before();
+                    } else {
+                        const double* t = myhold + (size_t)(ps - SQ) * HSLOT + lane;
+#pragma unroll 8
+                        for (int c = 0; c < CS; c += 2) {
+                            const double2 d2 = *reinterpret_cast<const double2*>(dxv + c);
+                            s4[c & 3] = fma(t[c * 32], d2.x, s4[c & 3]);
+                            s4[(c + 1) & 3] = fma(t[(c + 1) * 32], d2.y, s4[(c + 1) & 3]);
+                        }
+                    }
+                    const double part = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                    if (srow < rows) {
+                        if (NSPLIT == 1) rs[srow] += part;
+                        else if (h == 0) delta[srow] = part;
+                        else if (h < NSPLIT - 1) delta[srow] += part;
+                        else rs[srow] += delta[srow] + part;  // the whole block update at once
+                    }
+                    __syncwarp();
+                    ++fin;
+                    if (lane == 0) st_release_cta_u32(&parked_done[a], fin);
+                }
+                pslot += cnt;
+                if (pslot >= np) pslot -= np;
+            } else if (h == NSPLIT - 1) {
+                // (a block narrower than the split: its update is complete in delta)
+                for (int i = 0; i < cnt; ++i) {
+                    const int srow = 32 * (a + kSlabDot * i) + lane;
+                    if (srow < rows) rs[srow] += delta[srow];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&dxempty[xp.i]);
+                if (h == NSPLIT - 1) st_release_cta_u64(&progress[a], (unsigned long long)(k + 1));
+            }
+            xp.next();
+            sp.mark(4);
+        }
+    } else {
+        slab_sequence_warp<BMAX, NSPLIT>(P, warp - kSlabSeq0, lane, pring, dxring, meta, pfull, pempty, dxfull,
+                                          dxempty, sp);
+    }
+    sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * kSlabWarps + warp) * 8 : nullptr, lane);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc_512(tmem_base);
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) P.r[row0 + i] = rs[i];
+}
+
+}  // namespace asy

@@ -18,6 +18,9 @@ def make_case(name):
     if name == "large_block":     # config 3 recipe, small, max block size 128
         return inputs.dense_lasso(300, 700, nnz_frac=0.005, sigma=0.01, lam_frac=0.02, block=128,
                                   gamma=0.9, seed=4)
+    if name == "tall_block":      # 280 rows: one worker's slab = 9 row groups of 128 columns
+        return inputs.dense_lasso(280, 520, nnz_frac=0.01, sigma=0.01, lam_frac=0.02, block=128,
+                                  gamma=0.9, seed=11)
     if name == "sparse_logistic":  # config 4 recipe, small
         P = inputs.sparse_logistic(300, 900, density=0.03, seed=6, lam_frac=0.1)
         s, e = P.colptr[100], P.colptr[101]          # make column 100 empty (edge case)

@@ -226,9 +226,13 @@ def test_async_long_launch_slot_reuse_ragged(A):
 
 
 DENSE_VARIANTS = {
-    "slab_hold": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_HOLD": "1"},   # axpy reads the dot pass's chunk
-    "slab_reload": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_HOLD": "0"},  # axpy re-loads the chunk (L2)
-    "slab_chunks": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_RC": "8"},    # many chunks per sequence
+    # smem / L2 form of the slab kernel
+    "slab_hold": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_HOLD": "1"},   # axpy reads the dot pass's chunk
+    "slab_reload": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_HOLD": "0"},  # axpy re-loads the chunk (L2)
+    "slab_chunks": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_RC": "8"},    # many chunks per sequence
+    # TMEM-parking form of the slab kernel (dense_slabt.cuh)
+    "slabt": {"ASY_DENSE_KERNEL": "slab"},
+    "slabt_nsw2": {"ASY_DENSE_KERNEL": "slab", "ASY_SLABT_NSW": "2"},
     "panel": {"ASY_DENSE_KERNEL": "panel"},           # TMEM panel kernel
     "panel_reread": {"ASY_DENSE_KERNEL": "panel", "ASY_NO_TMEM": "1"},
 }
@@ -260,11 +264,13 @@ def test_dense_kernel_variants(A, case, variant, monkeypatch):
         S.close()
 
 
-@pytest.mark.parametrize("kernel", ["slab", "panel"])
+@pytest.mark.parametrize("kernel", ["slab", "slab_smem", "panel"])
 @pytest.mark.parametrize("workers", [1, 3, 37])
 def test_dense_few_workers(A, workers, kernel, monkeypatch):
     """Fewer CTAs than SMs (taller row slabs / fewer panel workers), same results."""
-    monkeypatch.setenv("ASY_DENSE_KERNEL", kernel)
+    monkeypatch.setenv("ASY_DENSE_KERNEL", kernel.split("_")[0])
+    if kernel == "slab_smem":
+        monkeypatch.setenv("ASY_SLAB_TMEM", "0")
     P = make_case("dense_ragged")
     S = A.Solver(P)
     try:
@@ -275,6 +281,36 @@ def test_dense_few_workers(A, workers, kernel, monkeypatch):
         x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
         out = S.stationarity()
         assert _rel_f(out.objective, F_star) <= 1e-6 and out.mf_norm2 <= 1e-5
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("case,workers", [("tall_block", 1), ("large_block", 2), ("large_block", 3), ("large_block", 7),
+                                          ("dense_ragged", 1), ("dense_ragged", 2), ("nonconvex", 1),
+                                          ("dense_logistic", 1)])
+def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
+    """TMEM-parking slab kernel with tall slabs: several 32-row groups per dot warp, a ragged
+    last group (1-D bulk copies), hold slots in shared memory when a warp owns more groups than
+    its TMEM lane quarter holds (tall_block, 1 worker: 9 groups of 128 columns), park rings
+    that wrap many times.  Sequential parity per sweep, then asynchronous convergence."""
+    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    P = make_case(case)
+    S = A.Solver(P)
+    try:
+        for sweeps in (1, 3):
+            st = S.solve(sweeps=sweeps, max_delay=0, reset=True, workers=workers)
+            assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
+            x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, sweeps))
+            assert _rel_x(S.x(), x_or) <= REL
+        x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
+        S.solve(sweeps=0, reset=True)
+        for _ in range(60):
+            S.solve(sweeps=100, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=3)
+            out = S.stationarity()
+            meas = out.merit_inf if P.c > 0 else out.mf_norm2
+            if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
+                break
+        assert _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5
     finally:
         S.close()
 

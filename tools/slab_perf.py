@@ -22,7 +22,8 @@ for v in variants:
         os.environ[k] = val
         keys.append(k)
     for rep in range(2):
-        st = S.solve(sweeps=sw, reset=True, schedule=A.ASY_SCHED_RANDOM, seed=rep)
+        st = S.solve(sweeps=sw, reset=True, schedule=A.ASY_SCHED_RANDOM, seed=rep,
+                     workers=int(os.environ.get("WORKERS", "0")))
         gbs = 8.0 * P.m * P.n * sw / (st.kernel_ms * 1e-3) / 1e9
         print(f"{name:>12s} rep {rep}: {st.kernel_ms:8.3f} ms  {gbs:8.1f} GB/s  "
               f"{P.nblocks * sw / (st.kernel_ms * 1e-3) / 1e6:7.3f} M upd/s  F {st.objective:.10e}", flush=True)
