@@ -748,7 +748,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     const int64_t m = h->m, B = h->B;
     if (B > 128) return false;
     const int bmax = B <= 32 ? 32 : B <= 64 ? 64 : 128;
-    const int nsplit = bmax > 64 ? 2 : 1, CS = bmax / nsplit, SQ = 256 / CS;
+    const int CS = 32, nsplit = bmax / CS, SQ = 256 / CS;  // 32-column sub-sequences, 8 TMEM slots per quarter
     // slabs of whole 32-row groups: ngt groups over the CTAs, ngt / grid or one more each
     const int64_t ngt = (m + 31) / 32;
     int64_t grid0 = h->sms;
@@ -757,16 +757,6 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     const int nrg = (int)((ngt + grid0 - 1) / grid0);  // most groups of a CTA
     const int64_t Rs = 32 * (int64_t)nrg;
     if ((nrg + kSlabDot - 1) / kSlabDot > kSlabTMaxG) return false;
-    int extra = 0;  // extra hold slots per warp (measurement knob)
-    if (const char* e = getenv("ASY_SLABT_EXTRA")) extra = std::max(0, atoi(e));
-    int nhold = 0;
-    for (int d = 0; d < kSlabDot; ++d) {
-        const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
-        const int hs = std::max(0, nsplit * cnt - SQ) + (cnt > 0 ? extra : 0);
-        g->hoff[d] = nhold;
-        g->npark[d] = SQ + hs;
-        nhold += hs;
-    }
     const size_t unit = sizeof(double) * 32 * 16, hslot = sizeof(double) * 32 * CS;
     const int64_t RsP = (Rs + 1) & ~1ll;
     const size_t fixed = sizeof(double) * (3 * RsP + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
@@ -774,11 +764,28 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
                          sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 2 * kSlabNDX) +
                          sizeof(unsigned long long) * kSlabAx + sizeof(unsigned) * (kSlabDot + 1) + 256;
     const size_t cap = 227 * 1024;
-    int nsw = kSlabTMaxStages / kSlabDot;
-    if (const char* e = getenv("ASY_SLABT_NSW")) nsw = std::max(1, std::min(nsw, atoi(e)));
-    while (nsw >= 4 && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
-    if (nsw < 4 && !getenv("ASY_SLABT_NSW")) return false;
-    if (fixed + nhold * hslot + kSlabDot * nsw * unit > cap) return false;
+    // park ring of dot warp d: its groups of (nsplit + X) sub-sequences, X = spare sub-sequences
+    // (a warp may start sub-sequence (k+1, h) once the all-reduce of (k, h - X) freed its slots);
+    // the largest X <= 3 that leaves a load ring of >= 4 stages per warp
+    int xmax = 3, xmin = 0;
+    if (const char* e = getenv("ASY_SLABT_EXTRA")) xmax = xmin = std::max(0, atoi(e));
+    int nsw = 0, nhold = 0;
+    for (int X = xmax; X >= xmin; --X) {
+        nhold = 0;
+        for (int d = 0; d < kSlabDot; ++d) {
+            const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
+            const int hs = std::max(0, (nsplit + X) * cnt - SQ);
+            g->hoff[d] = nhold;
+            g->npark[d] = SQ + hs;
+            nhold += hs;
+        }
+        nsw = kSlabTMaxStages / kSlabDot;
+        if (const char* e = getenv("ASY_SLABT_NSW")) nsw = std::max(1, std::min(nsw, atoi(e)));
+        while (nsw > 4 && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
+        if (fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
+        nsw = 0;
+    }
+    if (nsw == 0) return false;
     g->grid = (int)grid0;
     g->Rs = Rs; g->bmax = bmax; g->nsw = nsw; g->nhold = nhold;
     g->smem = fixed + nhold * hslot + kSlabDot * nsw * unit;
@@ -789,7 +796,7 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
                               int64_t delay, float* ms) {
     const int64_t B = h->B;
     delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
-    const int nsplit = geo.bmax > 64 ? 2 : 1;  // all-reduces per block update
+    const int nsplit = geo.bmax / 32;  // all-reduces per block update
     const int64_t slots = next_pow2(std::max<int64_t>(64, nsplit * (2 * delay + 2)));
     const int det = delay == 0 ? 1 : 0;
     h->last_kernel = ASY_KERNEL_DENSE_SLAB_TMEM;

@@ -141,7 +141,10 @@ struct StageMeta {
 };
 
 // clock64 segment profiler (debug): seg[i] += cycles since the previous mark
+// (compiled in only with -DASY_SEGPROF -- a profiling build, `build.py --variant prof
+// ASY_SEGPROF`, loaded with ASY_LIB_VARIANT=prof; otherwise every call is empty)
 struct SegProf {
+#ifdef ASY_SEGPROF
     unsigned long long seg[8];
     long long last;
     __device__ void start() {
@@ -157,6 +160,11 @@ struct SegProf {
         if (out && lane == 0)
             for (int i = 0; i < 8; ++i) out[i] = seg[i];
     }
+#else
+    __device__ void start() {}
+    __device__ void mark(int) {}
+    __device__ void flush(unsigned long long*, int) {}
+#endif
 };
 
 struct Handoff {

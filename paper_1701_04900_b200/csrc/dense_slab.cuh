@@ -187,7 +187,10 @@ __device__ __forceinline__ double slab_reduce8(double* v, int lane) {
     return t + __shfl_xor_sync(0xffffffffu, t, 16);
 }
 
+// (compiled in only with -DASY_SEGPROF -- a profiling build, `build.py --variant prof
+// ASY_SEGPROF`, loaded with ASY_LIB_VARIANT=prof; otherwise every call is empty)
 struct SlabProf {
+#ifdef ASY_SEGPROF
     unsigned long long seg[8];
     long long last;
     __device__ void start() {
@@ -203,6 +206,11 @@ struct SlabProf {
         if (out && lane == 0)
             for (int i = 0; i < 8; ++i) out[i] = seg[i];
     }
+#else
+    __device__ void start() {}
+    __device__ void mark(int) {}
+    __device__ void flush(unsigned long long*, int) {}
+#endif
 };
 
 // Per-sequence metadata, written once by the dot producer (the only thread that

@@ -10,17 +10,18 @@
 //     warp d own the groups g = d (mod 4) for the whole launch: they share one TMEM lane
 //     quarter (warp id mod 4), lane = row, and the axpy warp is the only writer of those
 //     rows of the residual slab, the dot warp their only reader besides it;
-//   * a block's columns are processed as NSPLIT "sub-sequences" of CS = BMAX / NSPLIT
-//     columns (CS = 64 for blocks of 65-128 columns, else the whole block): each has its
-//     own all-reduce, so the all-reduce of columns [0, 64) overlaps the loads of columns
-//     [64, 128).  The gradient of all sub-sequences is taken from ONE residual snapshot
+//   * a block's columns are processed as NSPLIT = BMAX / 32 "sub-sequences" of CS = 32
+//     columns: each has its own all-reduce, so the all-reduce of columns [0, 32) overlaps
+//     the loads and dot of the later columns, and a dot warp can start sub-sequence (k+1, h)
+//     as soon as the all-reduce of (k, h) (or an earlier one: spare park slots) has
+//     freed its park slots.  The gradient of all sub-sequences is taken from ONE residual snapshot
 //     (w = phi'(r) is computed once per sequence and kept in registers), and the axpy of
 //     the first sub-sequences goes to a pending buffer (delta) that is added to r together
 //     with the last one -- every residual row always holds whole block updates (reading
 //     R8 of DESIGN.md is unchanged);
 //   * slabs are whole 32-row groups (CTAs own ngt / grid or one more), so every unit is one
-//     2-D TMA box of 32 rows x 16 columns (4 KB); lanes 0-3 of warp 1 issue the four dot
-//     warps' unit streams in lockstep into per-warp rings of nsw stages.  Units are taken
+//     2-D TMA box of 32 rows x 16 columns (4 KB); lanes 0-7 of warp 1 issue the four dot
+//     warps' unit streams (two lanes per stream) in lockstep into per-warp rings of nsw stages.  Units are taken
 //     column block by column block across a warp's groups, so one butterfly reduction
 //     covers all its rows;
 //   * in the same pass over shared memory each unit is parked in its group's park slot
@@ -48,8 +49,8 @@ constexpr int kSlabTMaxG = 4;        // row groups per warp per sequence (slabs 
 template <int BMAX, int LOSS>
 __global__ void __launch_bounds__(kSlabThreads, 1)
     dense_slabt_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams P) {
-    constexpr int NSPLIT = BMAX > 64 ? 2 : 1;  // sub-sequences per block update
-    constexpr int CS = BMAX / NSPLIT;          // columns of a sub-sequence
+    constexpr int CS = 32;                     // columns of a sub-sequence
+    constexpr int NSPLIT = BMAX / CS;          // sub-sequences (all-reduces) per block update
     constexpr int SQ = 256 / CS;               // TMEM park slots per lane quarter (2*CS b32 columns)
     constexpr int UNIT = 32 * 16;              // doubles per unit stage (4 KB)
     constexpr int HSLOT = 32 * CS;             // doubles per smem hold slot
@@ -154,19 +155,33 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         sp.mark(0);
     } else if (warp == 1) {
         // ---------------------------------------------------------------- loads (all four dot rings)
-        // Lane d < 4 owns dot warp d's unit stream: for k, h < NSPLIT, 16-column block cb,
-        // i < cnt_d: rows of group d + 4 i, columns [b B + h CS + 16 cb, +16).  The four lanes
-        // run in lockstep and issue in the same instruction whenever their ring has a free
-        // stage (a thread sustains only ~1 bulk copy per ~450 ns, tools/mb_tma.cu), and no
-        // ring waits for another (a dot warp waiting for a park slot holds only its stages).
+        // Dot warp d's unit stream: for k, h < NSPLIT, 16-column block cb, i < cnt_d: rows of
+        // group d + 4 i, columns [b B + h CS + 16 cb, +16).  The issuing lanes run in lockstep
+        // and issue in the same instruction whenever their ring has a free stage (a thread
+        // sustains only ~1 bulk copy per ~450 ns, tools/mb_tma.cu), and no ring waits for
+        // another (a dot warp waiting for a park slot holds only its own stages).
         const int W = B < 16 ? B : 16;  // unit columns loaded
         const uint32_t box_bytes = 32u * (uint32_t)W * 8u;
         const uint64_t pol = policy_evict_first();
-        const int d = lane;
-        const int cnt = (lane < kSlabDot && nrg > d) ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
-        int ist = 0, first = 1, ih = 0, icb = 0, ii = 0;
+        // lanes (d, e), d = lane & 3, e = lane >> 2 < NL: ring d's units u = e (mod NL) go to
+        // stage u mod nsw (NL = 2 when nsw is even: eight issuing threads per SM)
+        const int NL = (nsw & 1) ? 1 : 2;
+        const int d = lane & (kSlabDot - 1), e = lane >> 2;
+        const int cnt = (e < NL && nrg > d) ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
+        int ist = e, first = 1, ih = 0, icb = 0, ii = 0;
         uint32_t iph = 0;
         int64_t ik = cnt > 0 ? 0 : K, icol0 = 0, icached = -1;
+        auto adv = [&]() {  // next unit of ring d
+            if (++ii == cnt) {
+                ii = 0;
+                const int bh = min(CS, B - ih * CS);
+                if (++icb == (bh <= 0 ? 0 : (bh + 15) >> 4)) {
+                    icb = 0;
+                    if (++ih == NSPLIT) { ih = 0; ++ik; }
+                }
+            }
+        };
+        if (cnt > 0 && e == 1) adv();
         for (;;) {
             const bool live = ik < K;
             if (!__any_sync(0xffffffffu, live)) break;
@@ -192,15 +207,10 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                 mbar_arrive_expect_tx(&dfull[st], box_bytes);
                 slab_tma_2d(dstage + (size_t)st * UNIT, &tmap, (int)(row0 + 32 * g), (int)(icol0 + ih * CS + icb * 16),
                             &dfull[st], pol);
-                if (++ist == nsw) { ist = 0; iph ^= 1u; first = 0; }
-                if (++ii == cnt) {
-                    ii = 0;
-                    const int bh = min(CS, B - ih * CS);
-                    if (++icb == (bh <= 0 ? 0 : (bh + 15) >> 4)) {
-                        icb = 0;
-                        if (++ih == NSPLIT) { ih = 0; ++ik; }
-                    }
-                }
+                ist += NL;
+                if (ist >= nsw) { ist -= nsw; iph ^= 1u; first = 0; }
+                adv();
+                if (NL == 2 && ik < K) adv();
             }
             if (!__any_sync(0xffffffffu, ok)) __nanosleep(32);
         }
