@@ -632,11 +632,11 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
     const int64_t slots = next_pow2(std::max<int64_t>(1024, 2 * (delay + 2)));
-    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * Bmax));
+    TRY(dev_alloc(h, h->gacc, sizeof(double) * 2 * slots * kPanelRep * Bmax));
     TRY(dev_alloc(h, h->dpart, sizeof(double) * G * Bmax));
-    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots));
-    TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots));
-    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk));
+    TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots * kCtrPad));
+    TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots * kCtrPad));
+    TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk * kCtrPad));
 
     DenseAsyncParams P{};
     P.A = P_<double>(h->A); P.lda = h->lda;
@@ -673,7 +673,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
         CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * geo.grid * 16 * 8, h->stream));
         P.prof = P_<unsigned long long>(prof);
     }
-    dense_async_init<<<grid_for(std::max<int64_t>(2 * slots * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
+    dense_async_init<<<grid_for(std::max<int64_t>(2 * slots * kPanelRep * Bmax, h->nblk), 256, 4 * h->sms), 256, 0, h->stream>>>(P);
     CKL();
     void* args[] = {&tmap, &P};
     CK(cudaEventRecord(h->ev[0], h->stream));

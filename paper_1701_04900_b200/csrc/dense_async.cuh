@@ -84,6 +84,17 @@ constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
 constexpr int kClaim = ASY_CLAIM;    // subtasks claimed per atomic
 constexpr int kSlotCols = 256;       // TMEM columns per parked panel
 constexpr unsigned long long kParkWaitNs = 20000;  // max wait for a TMEM slot before re-reading
+// Per-block all-reduce layout: panel p adds its partial into accumulator replica p mod
+// kPanelRep (G ~ 80 panels adding into one copy serialise on a few L2 slices); the solves sum
+// the replicas.  Counters polled by many warps sit one per 128-byte line (stride kCtrPad).
+#ifndef ASY_PANEL_REP
+#define ASY_PANEL_REP 1
+#endif
+#ifndef ASY_PANEL_PAD
+#define ASY_PANEL_PAD 32
+#endif
+constexpr int kPanelRep = ASY_PANEL_REP;
+constexpr int kCtrPad = ASY_PANEL_PAD;
 
 struct DenseAsyncParams {
     const double* A;  // for re-reads of panels that were not parked in TMEM
@@ -178,11 +189,11 @@ __global__ void dense_async_init(DenseAsyncParams P) {
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if (tid == 0) *P.counter = 0ull;
     for (int64_t s = tid; s < P.slots; s += nth) {
-        P.arrive[s] = 0u;
-        P.consumed[s] = 0u;
+        P.arrive[s * kCtrPad] = 0u;
+        P.consumed[s * kCtrPad] = 0u;
     }
-    for (int64_t i = tid; i < 2 * P.slots * P.Bmax; i += nth) P.gacc[i] = 0.0;
-    for (int64_t i = tid; i < P.nblk; i += nth) P.xver[i] = 0u;
+    for (int64_t i = tid; i < 2 * P.slots * kPanelRep * P.Bmax; i += nth) P.gacc[i] = 0.0;
+    for (int64_t i = tid; i < P.nblk; i += nth) P.xver[i * kCtrPad] = 0u;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
@@ -454,9 +465,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long kk = e[i].k, kd = kk - P.delay - 1;
-                    xv[i] = ld_relaxed_u32(&P.xver[e[i].b]);
-                    cs[i] = ld_relaxed_u32(&P.consumed[kk & (P.slots - 1)]);
-                    cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[kd & (P.slots - 1)]) : 0u;
+                    xv[i] = ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]);
+                    cs[i] = ld_relaxed_u32(&P.consumed[(kk & (P.slots - 1)) * kCtrPad]);
+                    cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[(kd & (P.slots - 1)) * kCtrPad]) : 0u;
                 }
                 // admit in claim order: a subtask never waits while an older one of this batch is
                 // held back.  Guards are observed with relaxed loads: the TMA reads residual rows
@@ -473,9 +484,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     const unsigned need_w = kd >= 0 ? (unsigned)((kd >> lgS) + 1) * Gu : 0u;  // seq kd complete
                     if (xv[i] < need_x || cs[i] < need_s || cw[i] < need_w) {
                         // relaxed polls (ld.acquire would invalidate the SM's L1 on every poll)
-                        spin_until_ge_relaxed(&P.xver[e[i].b], need_x);
-                        spin_until_ge_relaxed(&P.consumed[kk & (P.slots - 1)], need_s);
-                        if (kd >= 0) spin_until_ge_relaxed(&P.consumed[kd & (P.slots - 1)], need_w);
+                        spin_until_ge_relaxed(&P.xver[e[i].b * kCtrPad], need_x);
+                        spin_until_ge_relaxed(&P.consumed[(kk & (P.slots - 1)) * kCtrPad], need_s);
+                        if (kd >= 0) spin_until_ge_relaxed(&P.consumed[(kd & (P.slots - 1)) * kCtrPad], need_w);
                         fence_acqrel_gpu();
                     }
                     push(e[i]);
@@ -527,7 +538,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
-            double* gacc = P.gacc + (slot * 2 + ((k >> P.lg_slots) & 1)) * Bmax;
+            double* gacc = P.gacc + ((slot * 2 + ((k >> P.lg_slots) & 1)) * kPanelRep + (p % kPanelRep)) * Bmax;
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const double* pan = stages + st * STAGE;
@@ -624,7 +635,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             __syncwarp();
             sp.mark(4);
             // publish (the partials' red.adds drained during the parking pass)
-            if (lane == 0) red_add_release_u32(&P.arrive[slot], 1u);
+            if (lane == 0) red_add_release_u32(&P.arrive[slot * kCtrPad], 1u);
             // hand-off note (after publishing: waiting here can never hold back a block)
             if (e >= kRing) mbar_wait(re, (uint32_t)(((e / kRing) - 1) & 1));
             if (lane == 0) {
@@ -650,8 +661,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         auto complete = [&]() {
             if (pend_slot >= 0 && lane == 0) {
                 fence_acqrel_gpu();  // r red.adds, x / accumulator writes before the counts (one membar)
-                red_add_u32(&P.consumed[pend_slot], 1u);
-                red_add_u32(&P.xver[pend_b], 1u);
+                red_add_u32(&P.consumed[pend_slot * kCtrPad], 1u);
+                red_add_u32(&P.xver[pend_b * kCtrPad], 1u);
             }
             pend_slot = -1;
         };
@@ -674,8 +685,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long k = md.k, b = md.b, p = md.p;
             const long long slot = k & (P.slots - 1);
             const long long use = k >> P.lg_slots;
-            const double* gacc = P.gacc + (slot * 2 + (use & 1)) * Bmax;
-            double* gnext = P.gacc + (slot * 2 + ((use + 1) & 1)) * Bmax;
+            const double* gacc = P.gacc + (slot * 2 + (use & 1)) * kPanelRep * Bmax;        // replica 0
+            double* gnext = P.gacc + (slot * 2 + ((use + 1) & 1)) * kPanelRep * Bmax;     // replica 0
             const long long c0 = b * P.B;
             const int nc = (int)((P.n - c0) < P.B ? (P.n - c0) : P.B);
             const long long u = md.u;
@@ -699,11 +710,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 unsigned ok = 0;
                 // relaxed poll: everything read after it that other SMs wrote (accumulator, x) is
                 // read with strong L2 loads, so no L1 invalidation (acquire) is needed
-                if (lane == 0) ok = ld_relaxed_u32(&P.arrive[slot]) >= need;
+                if (lane == 0) ok = ld_relaxed_u32(&P.arrive[slot * kCtrPad]) >= need;
                 ok = __shfl_sync(0xffffffffu, ok, 0);
                 if (!ok) {
                     complete();
-                    if (lane == 0) spin_until_ge_relaxed(&P.arrive[slot], need);
+                    if (lane == 0) spin_until_ge_relaxed(&P.arrive[slot * kCtrPad], need);
                 }
             }
             __syncwarp();
@@ -722,7 +733,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll 1
                         for (long long qq = 0; qq < P.G; ++qq) gv[s4] += ld_relaxed_f64(&P.part[qq * Bmax + c]);
                     } else {
-                        gv[s4] = ld_relaxed_f64(&gacc[c]);
+                        double gr[kPanelRep];
+#pragma unroll
+                        for (int r = 0; r < kPanelRep; ++r) gr[r] = ld_relaxed_f64(&gacc[r * Bmax + c]);
+#pragma unroll
+                        for (int r = 0; r < kPanelRep; ++r) gv[s4] += gr[r];
                     }
                 }
             }
@@ -743,7 +758,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 if (c < Bpad) dv[c] = dd;
                 // the slot's next user accumulates into the other half: clear ALL Bmax entries
                 // (that user's block may be wider than this one, e.g. after the ragged last block)
-                if (!P.deterministic && c < Bmax) gnext[c] = 0.0;
+                // (replica r is cleared by panel r mod G: every replica by some panel)
+                if (!P.deterministic && c < Bmax)
+                    for (long long r = p; r < kPanelRep; r += P.G) gnext[r * Bmax + c] = 0.0;
                 nz |= dd != 0.0;
             }
             nz = __any_sync(0xffffffffu, nz);
