@@ -287,7 +287,8 @@ def test_dense_few_workers(A, workers, kernel, monkeypatch):
 
 @pytest.mark.parametrize("case,workers", [("tall_block", 1), ("large_block", 2), ("large_block", 3), ("large_block", 7),
                                           ("dense_ragged", 1), ("dense_ragged", 2), ("nonconvex", 1),
-                                          ("dense_logistic", 1)])
+                                          ("dense_logistic", 1), ("box64", 1), ("box64", 2), ("block100", 1),
+                                          ("block100", 3), ("block100", 0)])
 def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
     """TMEM-parking slab kernel with tall slabs: several 32-row groups per dot warp, a ragged
     last group (1-D bulk copies), hold slots in shared memory when a warp owns more groups than
