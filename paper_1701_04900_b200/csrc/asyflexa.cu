@@ -740,7 +740,7 @@ static SlabKernelFn slabt_kernel_for(int bmax, int loss) {
 // (TMEM + shared-memory hold slots: one whole sequence per dot warp) plus a load ring of
 // >= 4 units per dot warp does not fit on the SM, or a warp would own > kSlabTMaxG groups.
 struct SlabTGeom {
-    int grid, bmax, nsw, nhold, npark[4], hoff[4];
+    int grid, bmax, nsw, nhold, npark[4], hoff[4], rotate;
     int64_t Rs;
     size_t smem;
 };
@@ -761,19 +761,23 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     const int64_t RsP = (Rs + 1) & ~1ll;
     const size_t fixed = sizeof(double) * (3 * RsP + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
                          (sizeof(SeqMeta) + sizeof(long long)) * kSlabNM +
-                         sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 2 * kSlabNDX) +
-                         sizeof(unsigned long long) * kSlabAx + sizeof(unsigned) * (kSlabDot + 1) + 256;
+                         sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 3 * kSlabNDX) +
+                         sizeof(unsigned long long) * (kSlabAx + kSlabDot) + sizeof(unsigned) * (kSlabDot + 1) + 256;
     const size_t cap = 227 * 1024;
     // park ring of dot warp d: its groups of (nsplit + X) sub-sequences, X = spare sub-sequences
     // (a warp may start sub-sequence (k+1, h) once the all-reduce of (k, h - X) freed its slots);
     // the largest X <= 3 that leaves a load ring of >= 4 stages per warp
     int xmax = 3, xmin = 0;
     if (const char* e = getenv("ASY_SLABT_EXTRA")) xmax = xmin = std::max(0, atoi(e));
+    // the last, partial round of groups rotates over the warps (any warp may hold one of them)
+    g->rotate = 1;
+    if (const char* e = getenv("ASY_SLABT_ROTATE")) g->rotate = atoi(e) != 0;
     int nsw = 0, nhold = 0;
     for (int X = xmax; X >= xmin; --X) {
         nhold = 0;
         for (int d = 0; d < kSlabDot; ++d) {
-            const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
+            const int cnt = g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
+                                      : (nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0);
             const int hs = std::max(0, (nsplit + X) * cnt - SQ);
             g->hoff[d] = nhold;
             g->npark[d] = SQ + hs;
@@ -837,6 +841,7 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     P.slots = slots;
     P.A = P_<double>(h->A); P.lda = h->lda;
     for (int d = 0; d < 4; ++d) { P.npark[d] = geo.npark[d]; P.hoff[d] = geo.hoff[d]; }
+    P.rotate = geo.rotate;
     const char* pf = getenv("ASY_PROF");
     Dev prof;
     if (pf) {

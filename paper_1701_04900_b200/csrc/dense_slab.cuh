@@ -104,6 +104,7 @@ struct SlabParams {
     int64_t lda;
     int npark[4];      // park ring per dot warp d: TMEM slots (256 / BMAX) + its smem hold slots
     int hoff[4];       // first smem hold slot of dot warp d
+    int rotate;        // the slab's last, partial round of row groups rotates over the warps per sequence
 };
 
 __global__ void slab_init(SlabParams P) {
@@ -284,7 +285,7 @@ template <int BMAX, int NSPLIT = 1>
 __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, int lane, const double* pring,
                                                    double* dxring, const SeqMeta* meta, uint64_t* pfull,
                                                    uint64_t* pempty, uint64_t* dxfull, uint64_t* dxempty,
-                                                   SlabProf& sp) {
+                                                   SlabProf& sp, uint64_t* arrived = nullptr) {
     const int64_t K = P.K;
     const int B = (int)P.B;
     const int64_t S = P.slots;
@@ -335,8 +336,14 @@ __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, i
         if (lane == 0) red_release_gpu_u32(&P.arrive[slot * kArrivePad], 1u);
         sp.mark(2);
         // all CTAs' partials of sub-sequence s
-        if (lane == 0) spin_until_ge_relaxed_u32(&P.arrive[slot * kArrivePad], (unsigned)(use + 1) * grid);
-        __syncwarp();
+        if (arrived) {
+            // the CTA's watcher lane polls the arrival counters (one poller per CTA) and
+            // signals this warp's ring slot
+            mbar_wait(&arrived[q], ph);
+        } else {
+            if (lane == 0) spin_until_ge_relaxed_u32(&P.arrive[slot * kArrivePad], (unsigned)(use + 1) * grid);
+            __syncwarp();
+        }
         sp.mark(3);
         double g[PER], y[PER];
 #pragma unroll

@@ -6,10 +6,11 @@
 // freshness D4 [PAPER.md:233] enforced per CTA), organised so that HBM streams while
 // the all-reduces are in flight:
 //
-//   * the slab is cut into 32-row groups g (the last one ragged).  Dot warp d and axpy
-//     warp d own the groups g = d (mod 4) for the whole launch: they share one TMEM lane
-//     quarter (warp id mod 4), lane = row, and the axpy warp is the only writer of those
-//     rows of the residual slab, the dot warp their only reader besides it;
+//   * the slab is cut into 32-row groups g.  Dot warp d and axpy warp d share one TMEM lane
+//     quarter (warp id mod 4; lane = row) and own the groups g = d + 4 i of the full rounds
+//     for the whole launch; the groups of the last, partial round rotate over the warps
+//     from one block update to the next (balanced load), a per-group progress counter
+//     ordering their updates;
 //   * a block's columns are processed as NSPLIT = BMAX / 32 "sub-sequences" of CS = 32
 //     columns: each has its own all-reduce, so the all-reduce of columns [0, 32) overlaps
 //     the loads and dot of the later columns, and a dot warp can start sub-sequence (k+1, h)
@@ -73,8 +74,10 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     uint64_t* pempty = pfull + kSlabNP;           // NP
     uint64_t* dxfull = pempty + kSlabNP;          // NDX
     uint64_t* dxempty = dxfull + kSlabNDX;        // NDX
-    unsigned long long* progress = reinterpret_cast<unsigned long long*>(dxempty + kSlabNDX);  // kSlabAx
-    unsigned* parked_done = reinterpret_cast<unsigned*>(progress + kSlabAx);                   // kSlabDot
+    uint64_t* arrived = dxempty + kSlabNDX;       // NDX: all CTAs' partials of the slot's sub-sequence
+    unsigned long long* progress = reinterpret_cast<unsigned long long*>(arrived + kSlabNDX);  // kSlabAx
+    unsigned long long* xprog = progress + kSlabAx;   // kSlabDot: sequences applied to extra group e
+    unsigned* parked_done = reinterpret_cast<unsigned*>(xprog + kSlabDot);                     // kSlabDot
     uint32_t* tmem_base_s = parked_done + kSlabDot;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -86,6 +89,17 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     const int rows = (int)max((int64_t)0, min((int64_t)32 * nrg, P.m - row0));     // this CTA's slab rows
     const int64_t K = P.K, N = P.nblk;
     const int B = (int)P.B;
+    // Row groups of warp d in sequence k: the base groups d + 4 i (i < nb, fixed for the launch)
+    // and at most one of the slab's last, partial round ("extra" groups 4 nb + e, e < E), which
+    // goes to warp (e + k) mod 4 (rotate) or warp e.  A rotating group's rows are updated by a
+    // different axpy warp in each sequence: xprog[e] orders those updates and guards their reads.
+    const int nb = nrg / kSlabDot, E = nrg % kSlabDot;
+    auto extra_of = [&](int d, int64_t k) {  // extra group index e of warp d in sequence k, or -1
+        const int e = P.rotate ? ((d - (int)(k & 3)) & 3) : d;
+        return e < E ? e : -1;
+    };
+    auto cnt_of = [&](int d, int64_t k) { return nb + (extra_of(d, k) >= 0 ? 1 : 0); };
+    auto grp_of = [&](int d, int64_t k, int i) { return i < nb ? d + kSlabDot * i : kSlabDot * nb + extra_of(d, k); };
 
     // ---- init
     for (int64_t i = threadIdx.x; i < (int64_t)P.nst * UNIT + (int64_t)P.nsa * HSLOT; i += blockDim.x) dstage[i] = 0.0;
@@ -109,8 +123,10 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         for (int s = 0; s < kSlabNDX; ++s) {
             mbar_init(&dxfull[s], 1);
             mbar_init(&dxempty[s], kSlabAx);
+            mbar_init(&arrived[s], 1);
         }
         for (int a = 0; a < kSlabAx; ++a) progress[a] = 0ull;
+        for (int e = 0; e < kSlabDot; ++e) xprog[e] = 0ull;
         for (int d = 0; d < kSlabDot; ++d) parked_done[d] = 0u;
         mbar_fence_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
@@ -135,21 +151,53 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     SlabProf sp;
     sp.start();
     if (warp == 0) {
-        // ---------------------------------------------------------------- schedule (S.1)
+        // ---------------------------------------------------------------- schedule (S.1) + watcher
+        // Lane 0 alternates two non-blocking steps: (1) walk the schedule into the metadata
+        // ring, up to kSlabNM sequences ahead of the slowest axpy warp; (2) poll the arrival
+        // counter of the oldest sub-sequence not yet complete and, once all CTAs arrived,
+        // signal its sequence warp (mbarrier arrived[s mod 6]).  One poller per CTA: hundreds
+        // of warps polling the counters slow every all-reduce down (measured).
         if (lane == 0) {
             SlabSchedule sch;
             sch.init(N);
-            for (int64_t k = 0; k < K; ++k) {
-                const SeqMeta mk = sch.next(P, k);
-                // the metadata slot of sequence k - NM is free once its axpy is done
-                if (k >= kSlabNM) {
-                    for (int a = 0; a < kSlabAx; ++a)
-                        while (ld_acquire_cta_u64(&progress[a]) < (unsigned long long)(k - kSlabNM + 1)) __nanosleep(64);
+            const int64_t total = K * NSPLIT;
+            const int64_t S = P.slots;
+            int lgS = 0;
+            while (((int64_t)1 << lgS) < S) ++lgS;
+            const unsigned grid = gridDim.x;
+            int64_t ks = 0, sw = 0;
+            RingPos wp;
+            wp.init(kSlabNDX);
+            unsigned ns = 32;
+            while (ks < K || sw < total) {
+                bool moved = false;
+                if (ks < K) {
+                    bool room = true;
+                    if (ks >= kSlabNM)
+                        for (int a = 0; a < kSlabAx; ++a)
+                            room = room && ld_acquire_cta_u64(&progress[a]) >= (unsigned long long)(ks - kSlabNM + 1);
+                    if (room) {
+                        meta[ks & (kSlabNM - 1)] = sch.next(P, ks);
+                        asm volatile("st.release.cta.shared.b64 [%0], %1;" ::"r"(smem_u32(&meta_k[ks & (kSlabNM - 1)])),
+                                     "l"((long long)ks)
+                                     : "memory");
+                        ++ks;
+                        moved = true;
+                    }
                 }
-                meta[k & (kSlabNM - 1)] = mk;
-                asm volatile("st.release.cta.shared.b64 [%0], %1;" ::"r"(smem_u32(&meta_k[k & (kSlabNM - 1)])),
-                             "l"((long long)k)
-                             : "memory");
+                while (sw < total &&
+                       ld_relaxed_gpu_u32(&P.arrive[(sw & (S - 1)) * kArrivePad]) >= (unsigned)((sw >> lgS) + 1) * grid) {
+                    mbar_arrive(&arrived[wp.i]);
+                    wp.next();
+                    ++sw;
+                    moved = true;
+                }
+                if (moved) {
+                    ns = 32;
+                } else {
+                    __nanosleep(ns);
+                    if (ns < 128) ns <<= 1;
+                }
             }
         }
         sp.mark(0);
@@ -167,21 +215,29 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         // stage u mod nsw (NL = 2 when nsw is even: eight issuing threads per SM)
         const int NL = (nsw & 1) ? 1 : 2;
         const int d = lane & (kSlabDot - 1), e = lane >> 2;
-        const int cnt = (e < NL && nrg > d) ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;
         int ist = e, first = 1, ih = 0, icb = 0, ii = 0;
         uint32_t iph = 0;
-        int64_t ik = cnt > 0 ? 0 : K, icol0 = 0, icached = -1;
+        int64_t ik = e < NL ? 0 : K, icol0 = 0, icached = -1;
+        int cnt = 0;
+        auto skip = [&]() {  // to the next sequence in which warp d has groups
+            while (ik < K && (cnt = cnt_of(d, ik)) == 0) ++ik;
+        };
         auto adv = [&]() {  // next unit of ring d
             if (++ii == cnt) {
                 ii = 0;
                 const int bh = min(CS, B - ih * CS);
                 if (++icb == (bh <= 0 ? 0 : (bh + 15) >> 4)) {
                     icb = 0;
-                    if (++ih == NSPLIT) { ih = 0; ++ik; }
+                    if (++ih == NSPLIT) {
+                        ih = 0;
+                        ++ik;
+                        skip();
+                    }
                 }
             }
         };
-        if (cnt > 0 && e == 1) adv();
+        skip();
+        if (ik < K && e == 1) adv();
         for (;;) {
             const bool live = ik < K;
             if (!__any_sync(0xffffffffu, live)) break;
@@ -203,7 +259,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                 }
             }
             if (ok) {
-                const int g = d + kSlabDot * ii;
+                const int g = grp_of(d, ik, ii);
                 mbar_arrive_expect_tx(&dfull[st], box_bytes);
                 slab_tma_2d(dstage + (size_t)st * UNIT, &tmap, (int)(row0 + 32 * g), (int)(icol0 + ih * CS + icb * 16),
                             &dfull[st], pol);
@@ -224,7 +280,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         uint64_t* myfull = dfull + d * nsw;
         uint64_t* myempty = dempty + d * nsw;
         const double* mystage = dstage + (size_t)d * nsw * UNIT;
-        const int cnt = nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0;  // my row groups
         // column blocks of sub-sequence h (blocks narrower than BMAX skip the empty ones)
         auto ncb_of = [&](int h) {
             const int bh = min(CS, B - h * CS);
@@ -238,6 +293,8 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         int pslot = 0;      // used mod np
         for (int64_t k = 0; k < K; ++k) {
             double w[kSlabTMaxG];
+            const int cnt = cnt_of(d, k);  // my row groups in sequence k
+            const int ex = extra_of(d, k);
             if (cnt > 0) {
                 // D1 / D4 guards: axpy(k - delay - 1) and axpy(kprev) applied to my rows
                 if (lane == 0) {
@@ -253,14 +310,18 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                 }
                 __syncwarp();
                 const int64_t need = meta[k & (kSlabNM - 1)].need;
-                if (need > 0)
-                    while (ld_acquire_cta_u64(&progress[d]) < (unsigned long long)need) __nanosleep(20);
+                if (need > 0) {
+                    if (nb > 0)
+                        while (ld_acquire_cta_u64(&progress[d]) < (unsigned long long)need) __nanosleep(20);
+                    if (ex >= 0)
+                        while (ld_acquire_cta_u64(&xprog[ex]) < (unsigned long long)need) __nanosleep(20);
+                }
                 sp.mark(1);
                 // one residual snapshot for the whole block update
 #pragma unroll
                 for (int i = 0; i < kSlabTMaxG; ++i) {
-                    const int srow = 32 * (d + kSlabDot * i) + lane;
-                    w[i] = (i < cnt && srow < rows) ? loss_prime_t<LOSS>(P.S, rs[srow], auxs[srow]) : 0.0;
+                    const int srow = i < cnt ? 32 * grp_of(d, k, i) + lane : rows;
+                    w[i] = srow < rows ? loss_prime_t<LOSS>(P.S, rs[srow], auxs[srow]) : 0.0;
                 }
             }
 #pragma unroll 1
@@ -340,7 +401,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         const uint32_t tq = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
         const int np = P.npark[a];
         const double* myhold = hold + (size_t)P.hoff[a] * HSLOT;
-        const int cnt = nrg > a ? (nrg - a + kSlabDot - 1) / kSlabDot : 0;
         RingPos xp;
         xp.init(kSlabNDX);
         unsigned fin = 0;
@@ -349,12 +409,16 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             const int64_t k = s / NSPLIT;
             const int h = (int)(s - k * NSPLIT);
             const int bh = min(CS, B - h * CS);
+            const int cnt = cnt_of(a, k), ex = extra_of(a, k);
             mbar_wait(&dxfull[xp.i], xp.ph);
             sp.mark(1);
+            // a rotating group: the previous sequence's update of its rows (another warp) first
+            if (h == 0 && ex >= 0)
+                while (ld_acquire_cta_u64(&xprog[ex]) < (unsigned long long)k) __nanosleep(20);
             const double* dxv = dxring + xp.i * CS;
             if (bh > 0) {
                 for (int i = 0; i < cnt; ++i) {
-                    const int srow = 32 * (a + kSlabDot * i) + lane;
+                    const int srow = 32 * grp_of(a, k, i) + lane;
                     double s4[4] = {0.0, 0.0, 0.0, 0.0};
                     int ps = pslot + i;
                     if (ps >= np) ps -= np;
@@ -400,21 +464,24 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             } else if (h == NSPLIT - 1) {
                 // (a block narrower than the split: its update is complete in delta)
                 for (int i = 0; i < cnt; ++i) {
-                    const int srow = 32 * (a + kSlabDot * i) + lane;
+                    const int srow = 32 * grp_of(a, k, i) + lane;
                     if (srow < rows) rs[srow] += delta[srow];
                 }
             }
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&dxempty[xp.i]);
-                if (h == NSPLIT - 1) st_release_cta_u64(&progress[a], (unsigned long long)(k + 1));
+                if (h == NSPLIT - 1) {
+                    if (ex >= 0) st_release_cta_u64(&xprog[ex], (unsigned long long)(k + 1));
+                    st_release_cta_u64(&progress[a], (unsigned long long)(k + 1));
+                }
             }
             xp.next();
             sp.mark(4);
         }
     } else {
         slab_sequence_warp<BMAX, NSPLIT>(P, warp - kSlabSeq0, lane, pring, dxring, meta, pfull, pempty, dxfull,
-                                          dxempty, sp);
+                                          dxempty, sp, arrived);
     }
     sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * kSlabWarps + warp) * 8 : nullptr, lane);
     tc_fence_before();
