@@ -60,7 +60,7 @@ namespace asy {
 
 constexpr int kPairs = 4;
 #ifndef ASY_AXPY_PER_PAIR
-#define ASY_AXPY_PER_PAIR 1
+#define ASY_AXPY_PER_PAIR 2
 #endif
 constexpr int kAxpyPerPair = ASY_AXPY_PER_PAIR;  // axpy warps per pair (2: hand-offs alternate)
 constexpr int kTmemSlots = 2;        // parked panels per pair (TMEM lane quarter = 2 x 256 columns)
@@ -76,7 +76,7 @@ constexpr int kRoll = ASY_ROLL;
 #define ASY_QUEUE 2
 #endif
 #ifndef ASY_CLAIM
-#define ASY_CLAIM 4
+#define ASY_CLAIM 4  // most subtasks claimed per atomic (runtime: DenseAsyncParams::claim)
 #endif
 constexpr int kQueue = ASY_QUEUE;    // scheduler -> producer queue depth
 constexpr int kRing = 32;            // hand-off notes per axpy warp
@@ -119,6 +119,7 @@ struct DenseAsyncParams {
     int deterministic;
     int use_tmem;     // park panels in TMEM when they fit (cols_per_panel <= kSlotCols)
     int keep_in_l2;   // blocks too large to park: load with L2 evict_normal so re-reads hit L2
+    int claim;        // subtasks claimed per atomic (1..kClaim)
     // synchronisation state (initialised by dense_async_init)
     unsigned long long* counter;
     double* gacc;        // [S][2][Bmax] accumulated A_b^T w; sequence k uses [k mod S][(k/S) & 1]
@@ -228,11 +229,17 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+#ifndef ASY_SPIN_MIN
+#define ASY_SPIN_MIN 32
+#endif
+#ifndef ASY_SPIN_MAX
+#define ASY_SPIN_MAX 256
+#endif
 __device__ __forceinline__ void spin_until_ge_relaxed(const unsigned* p, unsigned v) {
-    unsigned ns = 32;
+    unsigned ns = ASY_SPIN_MIN;
     while (ld_relaxed_u32(p) < v) {
         __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+        if (ns < ASY_SPIN_MAX) ns <<= 1;
     }
 }
 
@@ -431,15 +438,20 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int half = perm_half_bits(N);
             PermKeys pk{};
             long long ck = -1, cb = 0, cu = 0, cE = -1;  // cached sequence / block / epochs
-            long long tb = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
+            const int nclaim = P.claim;
+            long long tb = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
             while (tb < P.T) {
-                const long long tn = (long long)atomicAdd(P.counter, (unsigned long long)kClaim);
+                const long long tn = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
                 StageMeta e[kClaim];
                 unsigned xv[kClaim], cs[kClaim], cw[kClaim];
                 long long k = tb / G, p = tb - k * G;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long t = tb + i;
+                    if (i >= nclaim) {
+                        e[i].t = -1; e[i].k = 0; e[i].p = 0; e[i].b = 0; e[i].u = 0;
+                        continue;
+                    }
                     if (k != ck) {
                         ck = k;
                         cu = k / N;
@@ -465,6 +477,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     const long long kk = e[i].k, kd = kk - P.delay - 1;
+                    if (e[i].t < 0) { xv[i] = cs[i] = cw[i] = 0u; continue; }
                     xv[i] = ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]);
                     cs[i] = ld_relaxed_u32(&P.consumed[(kk & (P.slots - 1)) * kCtrPad]);
                     cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[(kd & (P.slots - 1)) * kCtrPad]) : 0u;
