@@ -1037,8 +1037,10 @@ static bool use_slab_kernel(const asy_handle* h) {
 
 static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
                                float* ms) {
+    void (*kern)(SparseAsyncParams) =
+        h->S.loss == LOSS_LS ? sparse_async_kernel<LOSS_LS> : sparse_async_kernel<LOSS_LOGISTIC>;
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sparse_async_kernel, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, 256, 0));
     int grid = std::max(1, occ) * h->sms;
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
     const int64_t slots = next_pow2(std::max<int64_t>(1 << 20, 2 * (delay + 2)));
@@ -1057,7 +1059,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     CKL();
     void* args[] = {&P};
     CK(cudaEventRecord(h->ev[0], h->stream));
-    CK(cudaLaunchCooperativeKernel((void*)sparse_async_kernel, dim3(grid), dim3(256), args, 0, h->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, 0, h->stream));
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();

@@ -37,6 +37,35 @@ struct SparseAsyncParams {
     int chunk;
 };
 
+__device__ __forceinline__ unsigned ld_relaxed_u32_g(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ long long ld_relaxed_s64_g(const long long* p) {
+    long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_relaxed_u32_g(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// relaxed polls (an acquire per poll would invalidate the SM's L1); the caller fences once
+__device__ __forceinline__ void spin_relaxed_u32_g(const unsigned* p, unsigned v) {
+    unsigned ns = 32;
+    while (ld_relaxed_u32_g(p) < v) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+}
+__device__ __forceinline__ void spin_relaxed_s64_g(const long long* p, long long v) {
+    unsigned ns = 32;
+    while (ld_relaxed_s64_g(p) < v) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+}
+
 __global__ void sparse_async_init(SparseAsyncParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -45,52 +74,98 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
     for (int64_t j = tid; j < P.n; j += nth) P.ver[j] = 0u;
 }
 
+// One block update's dependency chain is a few L2 round trips, so the kernel is arranged
+// to issue independent loads together: the guard loads, colptr, and (after colptr) the
+// column's row indices / values and x_j, tau_j are in flight at once; the residual is
+// gathered only after the guards passed.  No 64-bit division per update (the epoch and
+// position advance incrementally), one fence per update (after the scatter, before the
+// version / window counters), the loss fixed at compile time.
+template <int LOSS>
 __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 3, gl = lane & 7;
     const unsigned gmask = 0xFFu << (grp * 8);
+    const int64_t N = P.n;
+    const int half = perm_half_bits(N);
+    PermKeys pk{};
+    int64_t pkE = -1;
     for (;;) {
         long long base = 0;
         if (lane == 0) base = (long long)atomicAdd(P.counter, (unsigned long long)P.chunk);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= P.K) break;
         const long long kend = (base + P.chunk) < P.K ? (base + P.chunk) : P.K;
-        for (long long k = base + grp; k < kend; k += 4) {
-            const long long j = schedule_block(P.sched, P.seed, P.n, P.epoch0 * P.n + k);
+        // local epoch u and position i of this group's first sequence (one division per chunk)
+        long long k = base + grp;
+        int64_t u = k / N, i = k - u * N;
+        for (; k < kend; k += 4) {
+            int64_t j = i;
+            if (P.sched == SCHED_RANDOM) {
+                const int64_t E = P.epoch0 + u;
+                if (E != pkE) { pk = perm_keys(P.seed, E); pkE = E; }
+                uint64_t v = (uint64_t)i;
+                do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
+                j = (int64_t)v;
+            }
+            // guards (lane 0 of the group) and the column's extent, in flight together
+            const long long kd = k - P.delay - 1;
+            unsigned vj = 0;
+            long long dn = 0;
             if (gl == 0) {
-                spin_until_ge_u32(&P.ver[j], (unsigned)(k / P.n));                 // D4
-                const long long kd = k - P.delay - 1;
-                if (kd >= 0) spin_until_ge(&P.done[kd & (P.slots - 1)], kd);      // D1 window
+                vj = ld_relaxed_u32_g(&P.ver[j]);
+                if (kd >= 0) dn = ld_relaxed_s64_g(&P.done[kd & (P.slots - 1)]);
+            }
+            const int64_t s = __ldg(&P.colptr[j]), e = __ldg(&P.colptr[j + 1]);
+            // this lane's first nonzero and the block's x / tau (x_j final once ver[j] == u)
+            int32_t row0 = 0;
+            double val0 = 0.0;
+            if (s + gl < e) {
+                row0 = __ldg(&P.rowidx[s + gl]);
+                val0 = __ldg(&P.vals[s + gl]);
+            }
+            double tj = 0.0;
+            if (gl == 0) {
+                tj = __ldg(&P.tau[j]);
+                bool waited = false;
+                if (vj < (unsigned)u) { spin_relaxed_u32_g(&P.ver[j], (unsigned)u); waited = true; }   // D4
+                if (kd >= 0 && dn < kd) { spin_relaxed_s64_g(&P.done[kd & (P.slots - 1)], kd); waited = true; }  // D1
+                if (waited) asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             __syncwarp(gmask);
-            const int64_t s = P.colptr[j], e = P.colptr[j + 1];
+            double xj = 0.0;
+            if (gl == 0) xj = ld_relaxed_f64(&P.x[j]);
+            // gradient: sum_q a_qj phi'(r_q) over the column (inconsistent read of r)
             double acc = 0.0;
-            for (int64_t q = s + gl; q < e; q += 8) {
-                const int32_t row = P.rowidx[q];
-                acc = fma(P.vals[q], loss_prime(P.S, ld_relaxed_f64(&P.r[row]), P.aux[row]), acc);
+            if (s + gl < e) acc = val0 * loss_prime_t<LOSS>(P.S, ld_relaxed_f64(&P.r[row0]), __ldg(&P.aux[row0]));
+            for (int64_t q = s + gl + 8; q < e; q += 8) {
+                const int32_t row = __ldg(&P.rowidx[q]);
+                acc = fma(__ldg(&P.vals[q]), loss_prime_t<LOSS>(P.S, ld_relaxed_f64(&P.r[row]), __ldg(&P.aux[row])), acc);
             }
             acc += __shfl_xor_sync(gmask, acc, 4);
             acc += __shfl_xor_sync(gmask, acc, 2);
             acc += __shfl_xor_sync(gmask, acc, 1);
             double d = 0.0;
             if (gl == 0) {
-                const double y = ld_relaxed_f64(&P.x[j]);
-                const double xh = best_response(P.S, acc, y, P.tau[j], j);
-                const double xn = y + P.gamma * (xh - y);
+                const double xh = best_response(P.S, acc, xj, tj, j);
+                const double xn = xj + P.gamma * (xh - xj);
                 P.x[j] = xn;
-                d = xn - y;
+                d = xn - xj;
             }
             d = __shfl_sync(gmask, d, grp * 8);
             if (d != 0.0) {
-                for (int64_t q = s + gl; q < e; q += 8) atomicAdd(&P.r[P.rowidx[q]], P.vals[q] * d);
-                __threadfence();
+                if (s + gl < e) atomicAdd(&P.r[row0], val0 * d);
+                for (int64_t q = s + gl + 8; q < e; q += 8) atomicAdd(&P.r[__ldg(&P.rowidx[q])], __ldg(&P.vals[q]) * d);
             }
             __syncwarp(gmask);
             if (gl == 0) {
-                __threadfence();
-                st_release_u32(&P.ver[j], (unsigned)(k / P.n) + 1u);
+                // the scatter and x_j before the counters (one fence; the group's atomics were
+                // ordered before it by the warp barrier)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                red_relaxed_u32_g(&P.ver[j], 1u);
                 atomicMax(&P.done[k & (P.slots - 1)], k);  // monotone: a late older seq never regresses it
             }
+            i += 4;
+            while (i >= N) { i -= N; ++u; }
         }
         __syncwarp();
     }
