@@ -1046,9 +1046,10 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     const int64_t slots = next_pow2(std::max<int64_t>(1 << 20, 2 * (delay + 2)));
     TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->n));
+    TRY(dev_alloc(h, h->rs, sizeof(double) * 2 * h->m));  // [r_i, aux_i] pairs for the launch
     SparseAsyncParams P{};
     P.colptr = P_<int64_t>(h->colptr); P.rowidx = P_<int32_t>(h->rowidx); P.vals = P_<double>(h->vals);
-    P.m = h->m; P.n = h->n; P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.x = P_<double>(h->x);
+    P.m = h->m; P.n = h->n; P.r = P_<double>(h->rs); P.aux = P_<double>(h->b); P.x = P_<double>(h->x);
     P.tau = P_<double>(h->tau); P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed;
     P.epoch0 = h->epochs; P.K = sweeps * h->n; P.delay = delay; P.counter = P_<unsigned long long>(h->counter);
     P.ver = P_<unsigned>(h->ver); P.done = P_<long long>(h->done); P.slots = slots;
@@ -1059,7 +1060,12 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     CKL();
     void* args[] = {&P};
     CK(cudaEventRecord(h->ev[0], h->stream));
+    sparse_pair_pack<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->r), P_<double>(h->b),
+                                                                             P_<double>(h->rs), h->m);
+    CKL();
     CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, 0, h->stream));
+    sparse_pair_unpack<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->rs), P_<double>(h->r), h->m);
+    CKL();
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();

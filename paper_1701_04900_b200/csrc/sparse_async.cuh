@@ -19,8 +19,8 @@ struct SparseAsyncParams {
     const int32_t* __restrict__ rowidx;
     const double* __restrict__ vals;
     int64_t m, n;
-    double* r;
-    const double* aux;
+    double* r;         // the residual's pair buffer [r_i, aux_i] (2 m doubles; r_i at 2 i)
+    const double* aux; // (unused by the kernel: aux_i is at r[2 i + 1])
     double* x;
     const double* tau;
     Scalars S;
@@ -47,6 +47,9 @@ __device__ __forceinline__ long long ld_relaxed_s64_g(const long long* p) {
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void red_relaxed_max_s64_g(long long* p, long long v) {
+    asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void red_relaxed_u32_g(unsigned* p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -66,6 +69,23 @@ __device__ __forceinline__ void spin_relaxed_s64_g(const long long* p, long long
     }
 }
 
+// residual and b / y interleaved for the launch (one 16-byte gather per nonzero), and back
+__global__ void sparse_pair_pack(const double* r, const double* aux, double* ry, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        ry[2 * i] = r[i];
+        ry[2 * i + 1] = aux[i];
+    }
+}
+__global__ void sparse_pair_unpack(const double* ry, double* r, int64_t m) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = ry[2 * i];
+}
+__device__ __forceinline__ double2 ld_relaxed_f64x2(const double* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
 __global__ void sparse_async_init(SparseAsyncParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -79,7 +99,8 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
 // column's row indices / values and x_j, tau_j are in flight at once; the residual is
 // gathered only after the guards passed.  No 64-bit division per update (the epoch and
 // position advance incrementally), one fence per update (after the scatter, before the
-// version / window counters), the loss fixed at compile time.
+// version / window counters; deferred to overlap the next update's loads), no returning
+// atomics on the path, the loss fixed at compile time.
 template <int LOSS>
 __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
@@ -89,6 +110,19 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
     const int half = perm_half_bits(N);
     PermKeys pk{};
     int64_t pkE = -1;
+    // completion of the group's previous update (fence, then its version and window counters),
+    // issued once the next update's first loads are in flight; never deferred across a wait
+    bool pend = false;
+    int64_t pj = 0;
+    long long pkk = 0;
+    auto flush = [&]() {
+        if (pend && gl == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // its scatter and x_j first
+            red_relaxed_u32_g(&P.ver[pj], 1u);
+            red_relaxed_max_s64_g(&P.done[pkk & (P.slots - 1)], pkk);  // monotone window counter
+        }
+        pend = false;
+    };
     for (;;) {
         long long base = 0;
         if (lane == 0) base = (long long)atomicAdd(P.counter, (unsigned long long)P.chunk);
@@ -126,20 +160,28 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
             double tj = 0.0;
             if (gl == 0) {
                 tj = __ldg(&P.tau[j]);
-                bool waited = false;
-                if (vj < (unsigned)u) { spin_relaxed_u32_g(&P.ver[j], (unsigned)u); waited = true; }   // D4
-                if (kd >= 0 && dn < kd) { spin_relaxed_s64_g(&P.done[kd & (P.slots - 1)], kd); waited = true; }  // D1
-                if (waited) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                const bool ok4 = vj >= (unsigned)u, ok1 = kd < 0 || dn >= kd;
+                if (!ok4 || !ok1) {
+                    flush();  // (the awaited update may be this group's pending one)
+                    if (!ok4) spin_relaxed_u32_g(&P.ver[j], (unsigned)u);                      // D4
+                    if (!ok1) spin_relaxed_s64_g(&P.done[kd & (P.slots - 1)], kd);             // D1
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
             }
+            flush();
             __syncwarp(gmask);
             double xj = 0.0;
             if (gl == 0) xj = ld_relaxed_f64(&P.x[j]);
             // gradient: sum_q a_qj phi'(r_q) over the column (inconsistent read of r)
             double acc = 0.0;
-            if (s + gl < e) acc = val0 * loss_prime_t<LOSS>(P.S, ld_relaxed_f64(&P.r[row0]), __ldg(&P.aux[row0]));
+            if (s + gl < e) {
+                const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)row0]);
+                acc = val0 * loss_prime_t<LOSS>(P.S, ra.x, ra.y);
+            }
             for (int64_t q = s + gl + 8; q < e; q += 8) {
                 const int32_t row = __ldg(&P.rowidx[q]);
-                acc = fma(__ldg(&P.vals[q]), loss_prime_t<LOSS>(P.S, ld_relaxed_f64(&P.r[row]), __ldg(&P.aux[row])), acc);
+                const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)row]);
+                acc = fma(__ldg(&P.vals[q]), loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
             }
             acc += __shfl_xor_sync(gmask, acc, 4);
             acc += __shfl_xor_sync(gmask, acc, 2);
@@ -153,20 +195,19 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
             }
             d = __shfl_sync(gmask, d, grp * 8);
             if (d != 0.0) {
-                if (s + gl < e) atomicAdd(&P.r[row0], val0 * d);
-                for (int64_t q = s + gl + 8; q < e; q += 8) atomicAdd(&P.r[__ldg(&P.rowidx[q])], __ldg(&P.vals[q]) * d);
+                if (s + gl < e) atomicAdd(&P.r[2 * (int64_t)row0], val0 * d);
+                for (int64_t q = s + gl + 8; q < e; q += 8)
+                    atomicAdd(&P.r[2 * (int64_t)__ldg(&P.rowidx[q])], __ldg(&P.vals[q]) * d);
             }
-            __syncwarp(gmask);
-            if (gl == 0) {
-                // the scatter and x_j before the counters (one fence; the group's atomics were
-                // ordered before it by the warp barrier)
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                red_relaxed_u32_g(&P.ver[j], 1u);
-                atomicMax(&P.done[k & (P.slots - 1)], k);  // monotone: a late older seq never regresses it
-            }
+            __syncwarp(gmask);  // (orders the group's atomics before lane 0's later fence)
+            pend = true;
+            pj = j;
+            pkk = k;
             i += 4;
             while (i >= N) { i -= N; ++u; }
         }
+        // before the warp-wide claim: another group of this warp may be waiting for it
+        flush();
         __syncwarp();
     }
 }
