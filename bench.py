@@ -136,7 +136,7 @@ def traffic_for(P):
         d = json.load(open(p)).get(P.name)
         if not d:
             return None
-        return d["dram_bytes_per_sweep"]
+        return d["dram_bytes_per_sweep"] + d.get("dram_write_bytes_per_sweep", 0.0)  # read + write
     except Exception:
         return None
 
