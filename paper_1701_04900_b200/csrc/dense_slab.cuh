@@ -285,7 +285,8 @@ template <int BMAX, int NSPLIT = 1>
 __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, int lane, const double* pring,
                                                    double* dxring, const SeqMeta* meta, uint64_t* pfull,
                                                    uint64_t* pempty, uint64_t* dxfull, uint64_t* dxempty,
-                                                   SlabProf& sp, uint64_t* arrived = nullptr) {
+                                                   SlabProf& sp, uint64_t* arrived = nullptr,
+                                                   const long long* meta_k = nullptr) {
     const int64_t K = P.K;
     const int B = (int)P.B;
     const int64_t S = P.slots;
@@ -300,6 +301,31 @@ __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, i
     for (int64_t s = q; s < K * NSPLIT; s += kSlabSeq, ph ^= 1u) {
         const int64_t k = s / NSPLIT;
         const int h = (int)(s - k * NSPLIT);
+        double tpre[PER];
+        bool have_tau = false;
+        if (meta_k) {
+            // metadata ready (flag): prefetch tau_b while the CTA's partial is computed
+            if (lane == 0) {
+                long long v;
+                for (;;) {
+                    asm volatile("ld.acquire.cta.shared.b64 %0, [%1];"
+                                 : "=l"(v)
+                                 : "r"(smem_u32(&meta_k[k & (kSlabNM - 1)]))
+                                 : "memory");
+                    if (v == k) break;
+                    __nanosleep(32);
+                }
+            }
+            __syncwarp();
+            const int64_t cb = (int64_t)meta[k & (kSlabNM - 1)].b * P.B + h * CS;
+            const int ncb = (int)max((int64_t)0, min(min((int64_t)CS, P.B - h * CS), P.n - cb));
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int cc = lane + 32 * e;
+                tpre[e] = cc < ncb ? __ldg(&P.tau[cb + cc]) : 1.0;
+            }
+            have_tau = true;
+        }
         // the CTA's partial (the dot warps' arrivals also publish the sequence's metadata)
         mbar_wait(&pfull[q], ph);
         sp.mark(1);
@@ -310,13 +336,12 @@ __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, i
         const int half = (int)(use & 1);
         const double* xr = (md.flags & 1) ? P.x1 : P.x0;
         double* xw = (md.flags & 1) ? P.x0 : P.x1;
-        double pv[PER], tpre[PER];
+        double pv[PER];
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
             const int cc = lane + 32 * e;
             const double* pw = pring + (size_t)q * kSlabDot * CS + cc;
             pv[e] = ((pw[0] + pw[CS]) + pw[2 * CS]) + pw[3 * CS];  // fixed order
-            tpre[e] = cc < nc ? P.tau[c0 + cc] : 1.0;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&pempty[q]);
@@ -334,6 +359,13 @@ __device__ __forceinline__ void slab_sequence_warp(const SlabParams& P, int q, i
         }
         __syncwarp();
         if (lane == 0) red_release_gpu_u32(&P.arrive[slot * kArrivePad], 1u);
+        if (!have_tau) {  // (after the release: it would wait for this load as well)
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int cc = lane + 32 * e;
+                tpre[e] = cc < nc ? __ldg(&P.tau[c0 + cc]) : 1.0;
+            }
+        }
         sp.mark(2);
         // all CTAs' partials of sub-sequence s
         if (arrived) {

@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         }
     } else {
         slab_sequence_warp<BMAX, NSPLIT>(P, warp - kSlabSeq0, lane, pring, dxring, meta, pfull, pempty, dxfull,
-                                          dxempty, sp, arrived);
+                                          dxempty, sp, arrived, meta_k);
     }
     sp.flush(P.prof ? P.prof + ((size_t)blockIdx.x * kSlabWarps + warp) * 8 : nullptr, lane);
     tc_fence_before();
