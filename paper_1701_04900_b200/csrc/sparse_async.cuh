@@ -101,8 +101,11 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
 // position advance incrementally), one fence per update (after the scatter, before the
 // version / window counters; deferred to overlap the next update's loads), no returning
 // atomics on the path, the loss fixed at compile time.
+#ifndef ASY_SPARSE_MINB
+#define ASY_SPARSE_MINB 1
+#endif
 template <int LOSS>
-__global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) {
+__global__ void __launch_bounds__(256, ASY_SPARSE_MINB) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 3, gl = lane & 7;
     const unsigned gmask = 0xFFu << (grp * 8);
@@ -132,24 +135,39 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
         // local epoch u and position i of this group's first sequence (one division per chunk)
         long long k = base + grp;
         int64_t u = k / N, i = k - u * N;
-        for (; k < kend; k += 4) {
-            int64_t j = i;
+        // the head of an update: its column (S.1), guard counters and column extent; the
+        // next update's head is loaded while the current one runs (counters are monotone, so an
+        // early read can only be stale-low: the guard then re-polls)
+        struct Head { int64_t j, s, e; unsigned vj; long long dn; };
+        auto head = [&](long long kk, int64_t ii, int64_t uu) {
+            Head hd;
+            hd.j = ii;
             if (P.sched == SCHED_RANDOM) {
-                const int64_t E = P.epoch0 + u;
+                const int64_t E = P.epoch0 + uu;
                 if (E != pkE) { pk = perm_keys(P.seed, E); pkE = E; }
-                uint64_t v = (uint64_t)i;
+                uint64_t v = (uint64_t)ii;
                 do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
-                j = (int64_t)v;
+                hd.j = (int64_t)v;
             }
-            // guards (lane 0 of the group) and the column's extent, in flight together
-            const long long kd = k - P.delay - 1;
-            unsigned vj = 0;
-            long long dn = 0;
+            const long long kd = kk - P.delay - 1;
+            hd.vj = 0;
+            hd.dn = 0;
             if (gl == 0) {
-                vj = ld_relaxed_u32_g(&P.ver[j]);
-                if (kd >= 0) dn = ld_relaxed_s64_g(&P.done[kd & (P.slots - 1)]);
+                hd.vj = ld_relaxed_u32_g(&P.ver[hd.j]);
+                if (kd >= 0) hd.dn = ld_relaxed_s64_g(&P.done[kd & (P.slots - 1)]);
             }
-            const int64_t s = __ldg(&P.colptr[j]), e = __ldg(&P.colptr[j + 1]);
+            hd.s = __ldg(&P.colptr[hd.j]);
+            hd.e = __ldg(&P.colptr[hd.j + 1]);
+            return hd;
+        };
+        Head nx{};
+        if (k < kend) nx = head(k, i, u);
+        for (; k < kend; k += 4) {
+            const Head cur = nx;
+            const int64_t j = cur.j, s = cur.s, e = cur.e;
+            const long long kd = k - P.delay - 1;
+            const unsigned vj = cur.vj;
+            const long long dn = cur.dn;
             // this lane's first two nonzeros (columns of up to 16 in one round trip; ~10 on
             // average in configs[4]) and the block's x / tau (x_j final once ver[j] == u)
             int32_t row0 = 0, row1 = 0;
@@ -162,13 +180,17 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
                 row1 = __ldg(&P.rowidx[s + gl + 8]);
                 val1 = __ldg(&P.vals[s + gl + 8]);
             }
+            const int64_t ucur = u;
+            i += 4;
+            while (i >= N) { i -= N; ++u; }
+            if (k + 4 < kend) nx = head(k + 4, i, u);
             double tj = 0.0;
             if (gl == 0) {
                 tj = __ldg(&P.tau[j]);
-                const bool ok4 = vj >= (unsigned)u, ok1 = kd < 0 || dn >= kd;
+                const bool ok4 = vj >= (unsigned)ucur, ok1 = kd < 0 || dn >= kd;
                 if (!ok4 || !ok1) {
                     flush();  // (the awaited update may be this group's pending one)
-                    if (!ok4) spin_relaxed_u32_g(&P.ver[j], (unsigned)u);                      // D4
+                    if (!ok4) spin_relaxed_u32_g(&P.ver[j], (unsigned)ucur);                   // D4
                     if (!ok1) spin_relaxed_s64_g(&P.done[kd & (P.slots - 1)], kd);             // D1
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 }
@@ -212,8 +234,6 @@ __global__ void __launch_bounds__(256) sparse_async_kernel(SparseAsyncParams P) 
             pend = true;
             pj = j;
             pkk = k;
-            i += 4;
-            while (i >= N) { i -= N; ++u; }
         }
         // before the warp-wide claim: another group of this warp may be waiting for it
         flush();
