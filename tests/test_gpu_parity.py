@@ -288,7 +288,7 @@ def test_dense_few_workers(A, workers, kernel, monkeypatch):
 @pytest.mark.parametrize("case,workers", [("tall_block", 1), ("large_block", 2), ("large_block", 3), ("large_block", 7),
                                           ("dense_ragged", 1), ("dense_ragged", 2), ("nonconvex", 1),
                                           ("dense_logistic", 1), ("box64", 1), ("box64", 2), ("block100", 1),
-                                          ("block100", 3), ("block100", 0)])
+                                          ("block100", 3), ("block100", 0), ("dc_exp", 1), ("dc_log", 2)])
 def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
     """TMEM-parking slab kernel with tall slabs: several 32-row groups per dot warp, a ragged
     last group (1-D bulk copies), hold slots in shared memory when a warp owns more groups than
@@ -312,6 +312,23 @@ def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
             if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
                 break
         assert _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5
+    finally:
+        S.close()
+
+
+@pytest.mark.parametrize("case,workers", [("tall_block", 1), ("large_block", 3), ("box64", 2), ("dense_ragged", 1)])
+def test_slab_tmem_sequential_random_schedule(A, case, workers, monkeypatch):
+    """TMEM slab kernel, sequential mode, seeded Philox/Feistel schedule: D4 through the inverse
+    permutation (schedule_prev) and the rotating partial round of groups, per-sweep parity."""
+    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    P = make_case(case)
+    S = A.Solver(P)
+    try:
+        st = S.solve(sweeps=3, max_delay=0, schedule=A.ASY_SCHED_RANDOM, seed=41, reset=True, workers=workers)
+        assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
+        x_or, _ = O.run_sequential(P, P.gamma, O.random_schedule(41, P.nblocks, 3))
+        assert _rel_x(S.x(), x_or) <= REL
+        assert _rel_f(S.objective(), O.objective(P, x_or)) <= REL
     finally:
         S.close()
 
