@@ -218,7 +218,7 @@ def run_ours(args, rank, world, local):
                 break
             st = S.solve(sweeps=args.check_every, **kw)
         stat = S.stationarity()
-        return updates, launches + 6, kms, sweeps, stat, st.kernel, st.delay
+        return updates, launches + 6, kms, sweeps, stat, st.kernel, st.delay, st.delay_observed
 
     for _ in range(args.warmup):
         solve_to_target({})
@@ -316,6 +316,7 @@ def run_ours(args, rank, world, local):
                          "frac": achieved / hbm_peak, "peak_kind": peak_kind,
                          "traffic": traffic, "kernel": A.KERNEL_NAMES.get(res[-1][5], "?"),
                          "enforced_delay": res[-1][6],
+                         "observed_delay": res[-1][7] if res[-1][7] >= 0 else None,
                          "bytes_per_sweep": bytes_per_sweep(P), "kernel_ms": kernel_ms / args.steps},
             "final": {"rel_err": (res[-1][4].objective - Fstar) / abs(Fstar), "mf_norm2": last_stat.mf_norm2,
                       "merit_inf": last_stat.merit_inf, "Fstar": Fstar, "Fstar_mf_norm2": st_star.mf_norm2},

@@ -147,6 +147,10 @@ typedef struct {
     int32_t kernel;          /* update kernel of the last launch: ASY_KERNEL_* */
     int32_t delay;           /* async: bounded delay actually enforced (<= max_delay; capped by the
                                 kernel's buffering), -1 for Jacobi */
+    int32_t delay_observed;  /* async, TMEM row-slab kernel: the largest number of earlier block
+                                updates missing from the residual rows a gradient was read from
+                                (observed delay, Assumption D1 [PAPER.md:224]; <= delay); -1 when the
+                                kernel that ran does not measure it */
 } asy_solve_stats;
 
 typedef struct {

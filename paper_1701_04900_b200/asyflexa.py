@@ -62,7 +62,7 @@ class asy_solve_params(C.Structure):
 class asy_solve_stats(C.Structure):
     _fields_ = [("block_updates", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double),
                 ("total_ms", C.c_double), ("objective", C.c_double), ("epochs", C.c_int64),
-                ("kernel", C.c_int32), ("delay", C.c_int32)]
+                ("kernel", C.c_int32), ("delay", C.c_int32), ("delay_observed", C.c_int32)]
 
 
 class asy_stationarity_out(C.Structure):

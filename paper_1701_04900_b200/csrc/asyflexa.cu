@@ -59,9 +59,11 @@ struct asy_handle {
     Dev red_part, red_out;                // reduction buffers
     // async state
     Dev counter, gacc, dpart, arrive, consumed, done, ver;
+    Dev dobs;                             // observed-delay statistic (u32)
     int64_t slots = 0;
     int64_t epochs = 0;                   // sweeps since reset (schedule epoch)
     int last_kernel = 0, last_delay = -1; // reported in asy_solve_stats
+    int last_dobs = -1;                   // observed delay of the last solve (-1: not measured)
 
     int fail(int code, const char* fmt, ...) {
         char buf[512];
@@ -142,7 +144,7 @@ static void free_problem(asy_handle* h) {
     Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
                   &h->tau, &h->lo, &h->hi, &h->x, &h->xalt, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
                   &h->part, &h->gacc, &h->dpart, &h->arrive, &h->consumed, &h->done,
-                  &h->ver};
+                  &h->ver, &h->dobs};
     for (Dev* d : all) dev_free(*d);
     h->has_problem = false;
 }
@@ -845,6 +847,9 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     P.A = P_<double>(h->A); P.lda = h->lda;
     for (int d = 0; d < 4; ++d) { P.npark[d] = geo.npark[d]; P.hoff[d] = geo.hoff[d]; }
     P.rotate = geo.rotate;
+    TRY(dev_alloc(h, h->dobs, sizeof(unsigned)));
+    CK(cudaMemsetAsync(h->dobs.p, 0, sizeof(unsigned), h->stream));
+    P.dobs = P_<unsigned>(h->dobs);
     const char* pf = getenv("ASY_PROF");
     Dev prof;
     if (pf) {
@@ -865,6 +870,11 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    {
+        unsigned dobs = 0;
+        CK(cudaMemcpy(&dobs, h->dobs.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        h->last_dobs = std::max(h->last_dobs, (int)dobs);
+    }
     if (sweeps & 1) std::swap(h->x, h->xalt);
     if (P.prof) {
         std::vector<unsigned long long> hb((size_t)geo.grid * kSlabWarps * 8);
@@ -1088,6 +1098,7 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     if (sp->stages < 0 || sp->stages > 16) return h->fail(ASY_ERR_INVALID, "stages must be in [0,16]");
     CK(cudaSetDevice(h->device));
     asy_solve_stats stats{};
+    h->last_dobs = -1;
     CK(cudaEventRecord(h->ev[2], h->stream));
     if (sp->reset) TRY(reset_state(h, sp->x0, sp->x_mem));
     int64_t delay = sp->max_delay;
@@ -1147,6 +1158,7 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     stats.epochs = h->epochs;
     stats.kernel = h->last_kernel;
     stats.delay = h->last_delay;
+    stats.delay_observed = h->last_dobs;
     if (st) *st = stats;
     return ASY_OK;
 }

@@ -105,6 +105,7 @@ struct SlabParams {
     int npark[4];      // park ring per dot warp d: TMEM slots (256 / BMAX) + its smem hold slots
     int hoff[4];       // first smem hold slot of dot warp d
     int rotate;        // the slab's last, partial round of row groups rotates over the warps per sequence
+    unsigned* dobs;    // max observed delay (earlier sequences missing from a read), atomicMax; may be null
 };
 
 __global__ void slab_init(SlabParams P) {

@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         cr.init(nsw);
         unsigned used = 0;  // park slots taken
         int pslot = 0;      // used mod np
+        long long dmax_local = 0;
         for (int64_t k = 0; k < K; ++k) {
             double w[kSlabTMaxG];
             const int cnt = cnt_of(d, k);  // my row groups in sequence k
@@ -315,6 +316,16 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                         while (ld_acquire_cta_u64(&progress[d]) < (unsigned long long)need) __nanosleep(20);
                     if (ex >= 0)
                         while (ld_acquire_cta_u64(&xprog[ex]) < (unsigned long long)need) __nanosleep(20);
+                }
+                // observed delay: the rows about to be read lack exactly sequences progress..k-1
+                if (lane == 0) {
+                    unsigned long long have = nb > 0 ? ld_acquire_cta_u64(&progress[d]) : (unsigned long long)k;
+                    if (ex >= 0) {
+                        const unsigned long long hx = ld_acquire_cta_u64(&xprog[ex]);
+                        if (hx < have) have = hx;
+                    }
+                    const long long miss = k - (long long)have;
+                    if (miss > dmax_local) dmax_local = miss;
                 }
                 sp.mark(1);
                 // one residual snapshot for the whole block update
@@ -395,6 +406,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                 sp.mark(4);
             }
         }
+        if (lane == 0 && P.dobs) atomicMax(P.dobs, (unsigned)dmax_local);
     } else if (warp < kSlabSeq0) {
         // ---------------------------------------------------------------- axpy warps
         const int a = warp - kSlabAx0;  // same TMEM lane quarter and rows as dot warp a

@@ -306,7 +306,8 @@ def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
         x_star, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
         S.solve(sweeps=0, reset=True)
         for _ in range(60):
-            S.solve(sweeps=100, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=3)
+            st = S.solve(sweeps=100, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=3)
+            assert 0 <= st.delay_observed <= st.delay  # Assumption D1 holds as enforced
             out = S.stationarity()
             meas = out.merit_inf if P.c > 0 else out.mf_norm2
             if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
@@ -326,6 +327,7 @@ def test_slab_tmem_sequential_random_schedule(A, case, workers, monkeypatch):
     try:
         st = S.solve(sweeps=3, max_delay=0, schedule=A.ASY_SCHED_RANDOM, seed=41, reset=True, workers=workers)
         assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
+        assert st.delay_observed == 0  # sequential: every read sees all earlier updates
         x_or, _ = O.run_sequential(P, P.gamma, O.random_schedule(41, P.nblocks, 3))
         assert _rel_x(S.x(), x_or) <= REL
         assert _rel_f(S.objective(), O.objective(P, x_or)) <= REL
