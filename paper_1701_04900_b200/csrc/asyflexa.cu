@@ -1050,7 +1050,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     void (*kern)(SparseAsyncParams) =
         h->S.loss == LOSS_LS ? sparse_async_kernel<LOSS_LS> : sparse_async_kernel<LOSS_LOGISTIC>;
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, kSparseThreads, 0));
     int grid = std::max(1, occ) * h->sms;
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
     const int64_t slots = next_pow2(std::max<int64_t>(1 << 20, 2 * (delay + 2)));
@@ -1073,7 +1073,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     sparse_pair_pack<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->r), P_<double>(h->b),
                                                                              P_<double>(h->rs), h->m);
     CKL();
-    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, 0, h->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSparseThreads), args, 0, h->stream));
     sparse_pair_unpack<<<grid_for(h->m, 256, 4 * h->sms), 256, 0, h->stream>>>(P_<double>(h->rs), P_<double>(h->r), h->m);
     CKL();
     CK(cudaEventRecord(h->ev[1], h->stream));

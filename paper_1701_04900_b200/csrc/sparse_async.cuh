@@ -104,8 +104,12 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
 #ifndef ASY_SPARSE_MINB
 #define ASY_SPARSE_MINB 1
 #endif
+#ifndef ASY_SPARSE_THREADS
+#define ASY_SPARSE_THREADS 128  // small CTAs: finer occupancy granularity at ~87 registers
+#endif
+constexpr int kSparseThreads = ASY_SPARSE_THREADS;
 template <int LOSS>
-__global__ void __launch_bounds__(256, ASY_SPARSE_MINB) sparse_async_kernel(SparseAsyncParams P) {
+__global__ void __launch_bounds__(kSparseThreads, ASY_SPARSE_MINB) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 3, gl = lane & 7;
     const unsigned gmask = 0xFFu << (grp * 8);
