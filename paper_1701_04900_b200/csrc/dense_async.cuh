@@ -12,7 +12,7 @@
 //
 // Warp roles.  Four "pairs" q = 0..3; pair q owns smem stage q and the TMEM
 // lane quarter [32q, 32q+32), split into two 256-column panel slots:
-//   warp 13 (lane 0)  scheduler: claims subtasks in batches of kClaim from the
+//   warp 13 (lane 0)  scheduler: claims subtasks in batches of P.claim (<= kClaim) from the
 //                     counter, checks the guards below (acquire) and queues the
 //                     admitted subtasks in shared memory;
 //   warp 12 (lane 0)  producer: pops the queue, arms the stage mbarrier and
