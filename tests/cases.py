@@ -21,6 +21,9 @@ def make_case(name):
     if name == "tall_block":      # 280 rows: one worker's slab = 9 row groups of 128 columns
         return inputs.dense_lasso(280, 520, nnz_frac=0.01, sigma=0.01, lam_frac=0.02, block=128,
                                   gamma=0.9, seed=11)
+    if name == "tall600":         # one worker's slab = 19 row groups: too tall for the TMEM park ring
+        return inputs.dense_lasso(600, 330, nnz_frac=0.02, sigma=0.01, lam_frac=0.05, block=32,
+                                  gamma=0.9, seed=14)
     if name == "box64":           # config 2 recipe, blocks of 64 (two 32-column sub-sequences)
         return inputs.nonconvex_box(150, 400, block=64, gamma=0.5, seed=12, lam_frac=0.3)
     if name == "block100":        # blocks of 100: padded to 128, last sub-sequence 4 columns wide

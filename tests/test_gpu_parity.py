@@ -335,6 +335,24 @@ def test_slab_tmem_sequential_random_schedule(A, case, workers, monkeypatch):
         S.close()
 
 
+def test_slab_fallback_when_too_tall(A, monkeypatch):
+    """A slab of 19 row groups (> 4 per dot warp) does not fit the TMEM park ring: the
+    dispatcher falls back to the smem/L2 slab form, with the same results."""
+    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    P = make_case("tall600")
+    S = A.Solver(P)
+    try:
+        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=1)
+        assert st.kernel == A.ASY_KERNEL_DENSE_SLAB and st.delay_observed == -1
+        x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 3))
+        assert _rel_x(S.x(), x_or) <= REL
+        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=8)  # 3 groups per slab: TMEM form
+        assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
+        assert _rel_x(S.x(), x_or) <= REL
+    finally:
+        S.close()
+
+
 def test_async_delay_window_respected_tiny(A):
     """configs[0] with all CTAs and an unbounded window diverges like Jacobi;
     the default window (N/8) converges (Theorem 1: gamma vs delta [PAPER.md:301])."""
