@@ -728,14 +728,14 @@ static SlabKernelFn slab_kernel_for(int cpw, int loss) {
 }
 
 // ---- row-slab kernel with the tile parked in TMEM (dense_slabt.cuh)
-static SlabKernelFn slabt_kernel_for(int bmax, int loss) {
+static SlabKernelFn slabt_kernel_for(int bmax, int cs, int loss) {
     if (loss == LOSS_LS) {
         if (bmax == 32) return dense_slabt_kernel<32, LOSS_LS>;
-        if (bmax == 64) return dense_slabt_kernel<64, LOSS_LS>;
+        if (bmax == 64) return cs == 64 ? dense_slabt_kernel<64, LOSS_LS, 64> : dense_slabt_kernel<64, LOSS_LS>;
         if (bmax == 128) return dense_slabt_kernel<128, LOSS_LS>;
     } else {
         if (bmax == 32) return dense_slabt_kernel<32, LOSS_LOGISTIC>;
-        if (bmax == 64) return dense_slabt_kernel<64, LOSS_LOGISTIC>;
+        if (bmax == 64) return cs == 64 ? dense_slabt_kernel<64, LOSS_LOGISTIC, 64> : dense_slabt_kernel<64, LOSS_LOGISTIC>;
         if (bmax == 128) return dense_slabt_kernel<128, LOSS_LOGISTIC>;
     }
     return nullptr;
@@ -745,7 +745,7 @@ static SlabKernelFn slabt_kernel_for(int bmax, int loss) {
 // (TMEM + shared-memory hold slots: one whole sequence per dot warp) plus a load ring of
 // >= 4 units per dot warp does not fit on the SM, or a warp would own > kSlabTMaxG groups.
 struct SlabTGeom {
-    int grid, bmax, nsw, nhold, npark[4], hoff[4], rotate;
+    int grid, bmax, nsw, nhold, npark[4], hoff[4], rotate, cs;
     int64_t Rs;
     size_t smem;
 };
@@ -753,7 +753,12 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     const int64_t m = h->m, B = h->B;
     if (B > 128) return false;
     const int bmax = B <= 32 ? 32 : B <= 64 ? 64 : 128;
-    const int CS = 32, nsplit = bmax / CS, SQ = 256 / CS;  // 32-column sub-sequences, 8 TMEM slots per quarter
+    // sub-sequence width: 32 columns (blocks of 65-128: four all-reduces per update overlap the
+    // later columns' loads), the whole block for blocks of 33-64 (one all-reduce per update)
+    int cs = bmax == 64 ? 64 : 32;
+    if (const char* e = getenv("ASY_SLABT_CS")) cs = (atoi(e) == 64 && bmax == 64) ? 64 : 32;
+    const int CS = cs, nsplit = bmax / CS, SQ = 256 / CS;
+    g->cs = cs;
     // slabs of whole 32-row groups: ngt groups over the CTAs, ngt / grid or one more each
     const int64_t ngt = (m + 31) / 32;
     int64_t grid0 = h->sms;
@@ -777,7 +782,12 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // the last, partial round of groups rotates over the warps (any warp may hold one of them)
     g->rotate = 1;
     if (const char* e = getenv("ASY_SLABT_ROTATE")) g->rotate = atoi(e) != 0;
+    // prefer a load ring of >= 8 stages per warp over spare park slots (configs[2]: 3.97 vs
+    // 3.74 TB/s); only then settle for >= 4 stages
     int nsw = 0, nhold = 0;
+    const char* nsw_env = getenv("ASY_SLABT_NSW");  // (measurement / test override of the ring depth)
+    const int min_first = nsw_env ? std::max(1, atoi(nsw_env)) : 8, min_last = nsw_env ? min_first : 4;
+    for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 4)
     for (int X = xmax; X >= xmin; --X) {
         nhold = 0;
         for (int d = 0; d < kSlabDot; ++d) {
@@ -790,8 +800,8 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
         }
         nsw = kSlabTMaxStages / kSlabDot;
         if (const char* e = getenv("ASY_SLABT_NSW")) nsw = std::max(1, std::min(nsw, atoi(e)));
-        while (nsw > 4 && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
-        if (fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
+        while (nsw > min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
+        if (nsw >= min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
         nsw = 0;
     }
     if (nsw == 0) return false;
@@ -805,12 +815,12 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
                               int64_t delay, float* ms) {
     const int64_t B = h->B;
     delay = std::min<int64_t>(delay, kSlabNM - 64);  // metadata ring depth
-    const int nsplit = geo.bmax / 32;  // all-reduces per block update
+    const int nsplit = geo.bmax / geo.cs;  // all-reduces per block update
     const int64_t slots = next_pow2(std::max<int64_t>(64, nsplit * (2 * delay + 2)));
     const int det = delay == 0 ? 1 : 0;
     h->last_kernel = ASY_KERNEL_DENSE_SLAB_TMEM;
     h->last_delay = (int)delay;
-    SlabKernelFn fn = slabt_kernel_for(geo.bmax, h->S.loss);
+    SlabKernelFn fn = slabt_kernel_for(geo.bmax, geo.cs, h->S.loss);
     if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no TMEM slab kernel for block size %lld", (long long)B);
     CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
     int occ = 0;
@@ -1033,7 +1043,7 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
 }
 
 // Which dense asynchronous kernel: the row-slab kernel when every SM's share of a block
-// update is large (>= 128 KB: tall and wide blocks, e.g. configs[3]); the TMEM panel
+// update is large (>= 64 KB: tall and wide blocks, e.g. configs[2] and [3]); the TMEM panel
 // kernel otherwise (a block update touches only G of the SMs, no global all-reduce per
 // update).  ASY_DENSE_KERNEL=panel|slab overrides (tests, measurements).
 static bool use_slab_kernel(const asy_handle* h) {
@@ -1041,8 +1051,10 @@ static bool use_slab_kernel(const asy_handle* h) {
         if (!strcmp(kv, "panel")) return false;
         if (!strcmp(kv, "slab")) return true;
     }
+    // (measured: configs[2], 69 KB per SM per update: slab 3.74 TB/s vs panel 3.22; configs[1],
+    // 17 KB: panel 4.4 vs slab 1.8)
     const double per_sm = 8.0 * (double)h->B * (double)h->m / (double)std::max(1, h->sms);
-    return per_sm >= 128.0 * 1024.0;
+    return per_sm >= 64.0 * 1024.0;
 }
 
 static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,

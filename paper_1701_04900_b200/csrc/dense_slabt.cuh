@@ -47,10 +47,10 @@ namespace asy {
 constexpr int kSlabTMaxStages = 64;  // 4 dot warps x nsw
 constexpr int kSlabTMaxG = 4;        // row groups per warp per sequence (slabs <= 512 rows)
 
-template <int BMAX, int LOSS>
+template <int BMAX, int LOSS, int CS_ = 32>
 __global__ void __launch_bounds__(kSlabThreads, 1)
     dense_slabt_kernel(const __grid_constant__ CUtensorMap tmap, const SlabParams P) {
-    constexpr int CS = 32;                     // columns of a sub-sequence
+    constexpr int CS = CS_;                    // columns of a sub-sequence (32, or 64 for blocks of 33-64)
     constexpr int NSPLIT = BMAX / CS;          // sub-sequences (all-reduces) per block update
     constexpr int SQ = 256 / CS;               // TMEM park slots per lane quarter (2*CS b32 columns)
     constexpr int UNIT = 32 * 16;              // doubles per unit stage (4 KB)
