@@ -23,7 +23,9 @@ Every function cites the PAPER.md passage it writes out.  Conventions
     [PAPER.md:437].
 
 Parity status: every function here is pinned by ``tests/test_oracle_pins.py``
-(closed forms, brute force, finite differences, sklearn, KKT invariants);
+(closed forms, brute force, finite differences, sklearn, KKT invariants, and
+the hand-derived M_F / merit / G / x0 / relative-error values of
+``tests/golden_cases.py``, derived in ``tests/golden/README.md``);
 none is "parity unpinned".
 """
 from __future__ import annotations

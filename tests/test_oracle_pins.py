@@ -315,3 +315,53 @@ def test_config0_oracle_converges():
     assert np.linalg.norm(O.stationarity(P, x)) <= 1e-9
     las = Lasso(alpha=P.lam / P.m, fit_intercept=False, tol=1e-14, max_iter=10 ** 6).fit(P.A, P.b)
     assert abs(O.objective(P, las.coef_) - O.objective(P, x)) <= 1e-10 * O.objective(P, x)
+
+
+# --------------------------------------------------------------------------- hand-derived M_F / merit / G / x0 / rel. error
+# (tests/golden_cases.py; derivations in tests/golden/README.md "1-D / 2-D stationarity pins")
+from golden_cases import MERIT_CASES, MF_CASES  # noqa: E402
+
+
+@pytest.mark.parametrize("name,P,x,want", MF_CASES, ids=[c[0] for c in MF_CASES])
+def test_stationarity_hand_derived(name, P, x, want):
+    """M_F of Eq. (5) [PAPER.md:287-290] with the box X active and with the DC shift
+    -lam grad h^-(x) of Eq. (13) [PAPER.md:534-541] at x != 0 (both signs)."""
+    got = O.stationarity(P, np.array(x, float))
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("name,P,x,want", MERIT_CASES, ids=[c[0] for c in MERIT_CASES])
+def test_merit_hand_derived(name, P, x, want):
+    """Nonzero values of the Sec. 4.3 merit ||hat x(x) - x||_inf [PAPER.md:549]."""
+    assert abs(O.merit_inf(P, np.array(x, float)) - want) <= 1e-15
+
+
+def test_G_indicator_outside_box():
+    """G = lam sum h(x_j) on X, +inf outside (problem (1) [PAPER.md:58-68], X_i closed convex)."""
+    from golden_cases import problem
+    P = problem(np.eye(2), [0.0, 0.0], lam=2.0, lo=-1.0, hi=1.0)
+    assert O.G(P, np.array([0.5, -1.0])) == 3.0
+    assert O.G(P, np.array([0.5, 1.5])) == math.inf
+    assert O.G(P, np.array([-1.0 - 1e-12, 0.0])) == math.inf
+    assert O.objective(P, np.array([2.0, 0.0])) == math.inf
+    Q = problem(np.eye(2), [0.0, 0.0], lam=1.0, lo=np.array([0.0, -3.0]), hi=np.array([1.0, -2.0]))
+    assert O.G(Q, np.array([0.5, -2.5])) == 3.0
+    assert O.G(Q, np.array([0.5, -1.5])) == math.inf
+
+
+def test_default_x0_is_projection_of_zero():
+    """x^0 = P_X(0) [PAPER.md:250]: a box that excludes 0 moves it to the nearer bound."""
+    from golden_cases import problem
+    assert list(O.default_x0(problem(np.eye(3), [0, 0, 0], lam=0.1, lo=0.2, hi=3.0))) == [0.2] * 3
+    assert list(O.default_x0(problem(np.eye(3), [0, 0, 0], lam=0.1, lo=-2.0, hi=-0.5))) == [-0.5] * 3
+    P = problem(np.eye(3), [0, 0, 0], lam=0.1, lo=np.array([0.25, -1.0, -4.0]), hi=np.array([1.0, 1.0, -3.0]))
+    assert list(O.default_x0(P)) == [0.25, 0.0, -3.0]
+
+
+def test_relative_error_definition():
+    """(F - F*)/|F*| of Sec. 4.2 [PAPER.md:451], including |F*| < 1 and F* < 0."""
+    assert O.relative_error(1.5, 0.5) == 2.0
+    assert O.relative_error(0.75, 0.25) == 2.0
+    assert O.relative_error(-0.9, -1.0) == pytest.approx(0.1, abs=1e-15)
+    assert O.relative_error(0.02, 0.01) == 1.0
+    assert O.relative_error(3.0, 3.0) == 0.0
