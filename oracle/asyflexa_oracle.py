@@ -35,7 +35,7 @@ from typing import Iterable, Optional
 
 import numpy as np
 import scipy.sparse as sp
-from scipy.special import expit
+from scipy.special import expit, xlogy
 
 # ----------------------------------------------------------------------------
 # data access (A as a linear operator; dense ndarray or scipy CSC)
@@ -380,3 +380,57 @@ def estimate_fstar(P, gamma: float, max_sweeps: int = 20000, tol: float = 1e-15,
 def relative_error(Fx: float, Fstar: float) -> float:
     """(F(x) - F*)/|F*| -- the 'relative error on the objective' of Sec. 4.2 [PAPER.md:451]."""
     return (Fx - Fstar) / abs(Fstar)
+
+
+# ----------------------------------------------------------------------------
+# certified F* for the convex l1 instances (Fenchel duality -- mathematics, not
+# the paper).  Used only to certify the F* of configs whose Algorithm 1 run is
+# too long for this CPU oracle (configs[4]: ~3e4 sweeps of 1e6 scalar blocks).
+# ----------------------------------------------------------------------------
+
+
+def dual_value_l1(P, x: np.ndarray) -> float:
+    """Fenchel dual value D(u) <= F* at the dual point built from x, for
+    F = f(Ax) + lam||x||_1 with no box, c = 0 and G = l1 (convex configs 0, 1, 3, 4).
+
+    min_x f(Ax) + lam||x||_1 has the dual max_u -f^*(u) s.t. ||A^T u||_inf <= lam.
+      LS, f(z) = s||z - b||^2:  f^*(u) = b^T u + ||u||^2/(4s);
+      logistic, f(z) = (1/m) sum log(1 + exp(-y_j z_j)), u = -(y o theta)/m,
+        theta in [0,1]^m:      f^*(u) = (1/m) sum theta log theta + (1-theta) log(1-theta).
+    The dual point is u0 = grad of f at Ax (LS: 2s(Ax - b); logistic:
+    theta = sigmoid(-y o Ax)) scaled by min(1, lam/||A^T u0||_inf) into the feasible set,
+    so F(x) - D(u) is a certified bound on F(x) - F* (weak duality)."""
+    if P.reg != "l1" or P.c != 0.0 or np.any(np.isfinite(lo_hi(P)[0])) or np.any(np.isfinite(lo_hi(P)[1])):
+        raise ValueError("dual_value_l1: convex l1 problems without a box only")
+    A = design(P)
+    z = A @ x
+    if P.loss == "ls":
+        u0 = 2.0 * P.scale * (z - P.b)
+        g = float(np.max(np.abs(A.T @ u0)))
+        u = u0 * (min(1.0, P.lam / g) if g > 0 else 1.0)
+        return float(-(P.b @ u) - (u @ u) / (4.0 * P.scale))
+    theta0 = expit(-P.b * z)
+    g = float(np.max(np.abs(A.T @ (P.b * theta0)))) / P.m
+    theta = theta0 * (min(1.0, P.lam / g) if g > 0 else 1.0)
+    ent = xlogy(theta, theta) + xlogy(1.0 - theta, 1.0 - theta)
+    return float(-np.sum(ent) / P.m)
+
+
+def duality_gap_l1(P, x: np.ndarray) -> float:
+    """F(x) - D(u(x)) >= F(x) - F* >= 0 (see dual_value_l1)."""
+    return objective(P, x) - dual_value_l1(P, x)
+
+
+def minimiser_l1_logistic_liblinear(P, tol: float = 1e-10) -> np.ndarray:
+    """Candidate minimiser of the convex l1-logistic F from an independent library
+    solver (scikit-learn / liblinear newGLMNET: min ||x||_1 + C sum log(1+exp(-y a_j x)),
+    C = 1/(m lam), which is F/lam).  Library primitive; its output is certified by
+    duality_gap_l1, never trusted on its own."""
+    import warnings
+    from sklearn.linear_model import LogisticRegression
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        lr = LogisticRegression(l1_ratio=1.0, C=1.0 / (P.m * P.lam), solver="liblinear",
+                                fit_intercept=False, tol=tol, max_iter=1000000)
+        lr.fit(sp.csr_matrix(design(P)), P.b)
+    return np.asarray(lr.coef_[0], float)

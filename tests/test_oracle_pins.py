@@ -365,3 +365,57 @@ def test_relative_error_definition():
     assert O.relative_error(-0.9, -1.0) == pytest.approx(0.1, abs=1e-15)
     assert O.relative_error(0.02, 0.01) == 1.0
     assert O.relative_error(3.0, 3.0) == 0.0
+
+
+# --------------------------------------------------------------------------- duality certificate (convex l1 configs)
+def test_dual_value_hand_derived():
+    """1-D LASSO 1/2(x-3)^2 + |x|: x* = 2, F* = 5/2, dual u* = -1, D = -b u - u^2/2 = 5/2;
+    from x the dual point is u0 = x - 3 scaled by min(1, 1/|u0|).
+    1-D logistic log(1+e^-x) + x/5 (m = 1, y = 1): x* = log 4, F* = log 5 - 1.6 log 2,
+    theta* = sigmoid(-x*) = 1/5 and D = -(0.2 log 0.2 + 0.8 log 0.8) = F*; from x = 0 the scaled
+    dual point is theta = 0.5 * min(1, 0.2/0.5) = 0.2, i.e. already the optimum."""
+    from golden_cases import problem
+    P = problem([[1.0]], [3.0], lam=1.0)
+    for x in (0.0, 1.0, 2.0):  # u0 = x - 3 <= -1: scaled to u = -1
+        assert abs(O.dual_value_l1(P, np.array([x])) - 2.5) <= 1e-15
+    assert abs(O.dual_value_l1(P, np.array([2.5])) - 1.375) <= 1e-15  # u = -1/2 feasible: 3/2 - 1/8
+    assert abs(O.dual_value_l1(P, np.array([5.0])) + 3.5) <= 1e-15    # u0 = 2 -> u = 1: -3 - 1/2
+    assert abs(O.duality_gap_l1(P, np.array([2.0]))) <= 1e-15
+    Q = inputs.Problem(name="lg1", kind="dense", m=1, n=1, loss="logistic", scale=1.0, b=np.array([1.0]),
+                       lam=0.2, tau=np.ones(1), block=1, gamma=1.0, A=np.ones((1, 1), order="F"))
+    Fstar = math.log(5.0) - 1.6 * math.log(2.0)
+    assert abs(O.objective(Q, np.array([math.log(4.0)])) - Fstar) <= 1e-15
+    for x in (0.0, 1.0, math.log(4.0)):
+        assert abs(O.dual_value_l1(Q, np.array([x])) - Fstar) <= 1e-15
+
+
+@pytest.mark.parametrize("kind", ["ls", "logistic"])
+def test_weak_duality_and_zero_gap_at_optimum(kind):
+    """D(u(x)) <= F* <= F(x) for arbitrary x (weak duality), and the gap closes at the
+    oracle's own Algorithm 1 limit (strong duality for these convex instances)."""
+    if kind == "ls":
+        P = inputs.dense_lasso(40, 90, nnz_frac=0.05, sigma=0.01, lam_frac=0.1, block=3, seed=21)
+    else:
+        P = inputs.sparse_logistic(80, 50, density=0.1, seed=22, lam_frac=0.05)
+    xs, Fs, _ = O.estimate_fstar(P, 1.0, max_sweeps=20000, tol=0.0)  # until F stops changing at all
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        x = rng.normal(scale=rng.choice([0.01, 1.0, 10.0]), size=P.n) * (rng.random(P.n) < 0.5)
+        assert O.dual_value_l1(P, x) <= Fs * (1 + 1e-12)
+        assert O.duality_gap_l1(P, x) >= -1e-12
+    # the gap of the gradient-built dual point is first order in ||x - x*|| (F - F* is second order)
+    assert O.duality_gap_l1(P, xs) <= (1e-9 if kind == "ls" else 1e-7) * abs(Fs)
+
+
+def test_dual_rejects_nonconvex_or_boxed():
+    P = inputs.nonconvex_box(10, 12, block=2, seed=1)
+    with pytest.raises(ValueError):
+        O.dual_value_l1(P, np.zeros(P.n))
+
+
+def test_liblinear_candidate_is_certified():
+    Q = inputs.sparse_logistic(120, 60, density=0.08, seed=1, lam_frac=0.05)
+    x = O.minimiser_l1_logistic_liblinear(Q)
+    xs, Fs, _ = O.estimate_fstar(Q, 1.0, max_sweeps=100000, tol=0.0)
+    assert O.duality_gap_l1(Q, x) <= 1e-7 * O.objective(Q, x)
+    assert abs(O.objective(Q, x) - Fs) <= 1e-8 * abs(Fs)

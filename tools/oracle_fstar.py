@@ -1,0 +1,68 @@
+"""Write tests/golden/fstar_full.json: the oracle's F* for BASELINE configs[1..4] at full size.
+
+Calls only oracle/ (and the seeded input recipe).  F* follows the paper: "run ... until
+variations in the objective value were undetectable" [PAPER.md:434] -- the oracle's
+sequential Algorithm 1 (d = 0, cyclic, the config's gamma) until a sweep changes F by at
+most 1e-15 relative (configs 1-3).  For the convex configs the Fenchel duality gap of the
+limit is recorded as a certificate (oracle.duality_gap_l1: F(x) - F* <= gap).  configs[4]
+(10^6 scalar blocks, ~3e4 sweeps to 1e-6 with tau = 0.25||a_j||^2/m + 1e-6) is beyond a
+CPU Algorithm 1 run, so its F* is F at a library solver's candidate minimiser
+(oracle.minimiser_l1_logistic_liblinear) certified by the same duality gap.
+
+usage: python tools/oracle_fstar.py 1 3 2 4     (merges into the JSON; ~1 h for configs[2])
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import asyflexa_oracle as O  # noqa: E402
+from paper_1701_04900_b200 import inputs  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden", "fstar_full.json")
+
+
+def fingerprint(P):
+    return {"m": P.m, "n": P.n, "block": P.block, "gamma": P.gamma, "lam": repr(P.lam),
+            "b_sum": repr(float(P.b.sum())), "tau_sum": repr(float(P.tau.sum()))}
+
+
+def run(idx):
+    t0 = time.time()
+    P = inputs.config(idx)
+    rec = {"fingerprint": fingerprint(P), "gen_s": time.time() - t0}
+    t1 = time.time()
+    if idx in (1, 2, 3):
+        x, F, sweeps = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
+        rec.update(method="oracle Algorithm 1 (d=0, cyclic) until |dF| <= 1e-15 |F| per sweep [PAPER.md:434]",
+                   sweeps=sweeps, converged=sweeps < 20000)
+    else:
+        x = O.minimiser_l1_logistic_liblinear(P, tol=1e-10)
+        F = O.objective(P, x)
+        rec.update(method="F at a liblinear candidate minimiser, certified by the Fenchel duality gap")
+    rec["F_star"] = repr(F)
+    if P.c == 0.0 and P.reg == "l1" and not (abs(P.lo) < float("inf")):
+        gap = O.duality_gap_l1(P, x)
+        rec["duality_gap"] = gap
+        rec["gap_rel"] = gap / abs(F)
+    else:
+        rec["merit_inf"] = O.merit_inf(P, x)
+    rec["solve_s"] = time.time() - t1
+    return rec
+
+
+if __name__ == "__main__":
+    for a in sys.argv[1:]:
+        idx = int(a)
+        rec = run(idx)
+        d = json.load(open(OUT)) if os.path.exists(OUT) else {
+            "citation": "F* of BASELINE configs[1..4] (seed 0) written by tools/oracle_fstar.py, which "
+                        "calls only oracle/; see its docstring and DESIGN.md reading R12."}
+        d[f"config{idx}"] = rec
+        with open(OUT + ".tmp", "w") as f:
+            json.dump(d, f, indent=1)
+        os.replace(OUT + ".tmp", OUT)
+        print(idx, rec, flush=True)
