@@ -2,16 +2,23 @@
 """Benchmark of the AsyFLEXA hot path on B200 (BASELINE.json metric:
 "block updates/sec and HBM GB/s vs peak; time to rel. objective err 1e-6").
 
-One step = one asynchronous solve of BASELINE configs[1] (dense LASSO,
-10000 x 20000 fp64, blocks of 32) from x0 = 0 until the relative objective
-error (F - F*)/|F*| <= 1e-6, checked every few sweeps from the maintained
-residual, followed by one stationarity evaluation (fresh residual, Eq. 5).
-`value` = block updates / s over the timed steps (device time, CUDA events,
-max over ranks); `ms_per_step` = time to rel. err 1e-6.
+One step = one asynchronous solve of a BASELINE config from x0 = P_X(0) until the
+north_star bar is met: relative objective error (F - F*)/|F*| <= 1e-6 (checked from the
+maintained residual every few sweeps) AND stationarity <= 1e-5 (||M_F||_2, Eq. 5; the
+Sec. 4.3 merit for the nonconvex configs[2], reading R11), the latter from a freshly
+recomputed residual -- every check inside the timed region.  F* is the oracle's
+(tests/golden/fstar_full.json, written by tools/oracle_fstar.py from oracle/ only).
 
---impl reference times the oracle (oracle/, plain fp64 CPU) on the host cores
-as the reference arm.  Multi-GPU: replicas only (independent instances, one
-per rank, seeds base+rank) -- the method has no data-path exchange.
+Headline (`value`, `ms_per_step`, `roofline`, `e2e`, `cpu_baseline`): configs[3], the
+largest single-GPU config (40000 x 100000 fp64, 32 GB).  `per_config` holds the same
+measurement for configs[1], [2] and [4] (N = 1 only), each with its own roofline, kernel
+and clocks.  `value` = block updates / s over the timed steps (device time, CUDA events,
+max over ranks); `ms_per_step` = time to the bar.  A solve that hits its sweep cap is
+reported with "reached": false and a null time to target.
+
+--impl reference times the oracle (oracle/, plain fp64 CPU) on the host cores as the
+reference arm.  Multi-GPU: replicas only (independent solves of the same instance, one
+per rank) -- the method has no data-path exchange.
 """
 from __future__ import annotations
 
@@ -24,28 +31,34 @@ import sys
 import threading
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-TARGET = 1e-6
+TARGET_REL = 1e-6
+TARGET_STAT = 1e-5
+METRIC = "block updates/sec (async AsyFLEXA) | HBM GB/s vs peak | time to rel. objective err 1e-6"
+# sweeps between objective checks and the sweep cap, per config
+CHECK = {0: 10, 1: 5, 2: 25, 3: 1, 4: 500}
+CAP = {0: 5000, 1: 2000, 2: 20000, 3: 500, 4: 150000}
+# per_config entries: (config, warmup, steps)
+EXTRA = [(1, 3, 10), (2, 2, 5), (4, 1, 3)]
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--extra", default=",".join(str(c) for c, _, _ in EXTRA),
+                    help="configs measured into per_config (N = 1 only; '' = none)")
     ap.add_argument("--schedule", default="cyclic", choices=["cyclic", "random"])
-    ap.add_argument("--check-every", type=int, default=5, help="sweeps between objective checks")
+    ap.add_argument("--check-every", type=int, default=0, help="sweeps between objective checks (0: per config)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--panel-rows", type=int, default=0)
-    ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--workers", type=int, default=0)
     return ap.parse_args()
 
@@ -63,11 +76,24 @@ def workload_name(P, schedule):
             f"async {schedule}, gamma {P.gamma}")
 
 
-def make_problem(idx, seed):
+def make_problem(idx):
     from paper_1701_04900_b200 import inputs
-    P = inputs.config(idx, seed=seed)
+    P = inputs.config(idx, seed=0)
     P.meta["config_idx"] = idx
     return P
+
+
+def golden_fstar(P, idx):
+    """The oracle's F* for configs[idx] (seed 0) and its certified slack, after checking the
+    instance fingerprint; None if there is no golden for this config."""
+    path = os.path.join(ROOT, "tests", "golden", "fstar_full.json")
+    g = json.load(open(path)).get(f"config{idx}") if os.path.exists(path) else None
+    if g is None:
+        return None, 0.0
+    fp = g["fingerprint"]
+    if (repr(P.lam), repr(float(P.b.sum()))) != (fp["lam"], fp["b_sum"]):
+        raise RuntimeError(f"configs[{idx}] instance differs from the golden F*'s fingerprint")
+    return float(g["F_star"]), float(g.get("duality_gap", 0.0)) if idx == 4 else 0.0
 
 
 def bytes_per_sweep(P):
@@ -125,20 +151,19 @@ def peaks():
     if os.path.exists(p):
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_for(P):
+def traffic_for(idx, kernel):
+    """DRAM read+write bytes per sweep of the update kernel from the committed ncu capture
+    of this config (profiles/traffic.json, per config and kernel), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
-        return None
-    try:
-        d = json.load(open(p)).get(P.name)
-        if not d:
-            return None
-        return d["dram_bytes_per_sweep"] + d.get("dram_write_bytes_per_sweep", 0.0)  # read + write
-    except Exception:
-        return None
+        return None, None
+    d = json.load(open(p)).get(f"configs[{idx}]")
+    if not d or d.get("kernel") != kernel:
+        return None, None
+    return d["dram_read_bytes_per_sweep"] + d["dram_write_bytes_per_sweep"], d["source"]
 
 
 def reduce_over_ranks(ms: float, units: float, world: int, device="cpu"):
@@ -156,7 +181,7 @@ def reduce_over_ranks(ms: float, units: float, world: int, device="cpu"):
 
 
 # ----------------------------------------------------------------------------- oracle arms
-def oracle_rate(P, seconds, x0=None):
+def oracle_rate(P, seconds):
     """Sequential Algorithm 1 (d = 0) of the oracle, as it stands, on host cores:
     block updates/s over a bounded sample (whole sweeps prefixes)."""
     from oracle import asyflexa_oracle as O
@@ -165,7 +190,7 @@ def oracle_rate(P, seconds, x0=None):
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
         cores = os.cpu_count()
-    x = None if x0 is None else x0.copy()
+    x = None
     done, t0 = 0, time.perf_counter()
     chunk = max(1, min(P.nblocks, 64))
     k = 0
@@ -179,6 +204,104 @@ def oracle_rate(P, seconds, x0=None):
 
 
 # ----------------------------------------------------------------------------- our arm
+class Target:
+    """Solve-to-the-bar loop through the public API (Solver.solve / Solver.stationarity)."""
+
+    def __init__(self, A, S, P, idx, Fstar, slack, kw, check):
+        self.A, self.S, self.P, self.idx = A, S, P, idx
+        self.Fstar, self.slack, self.kw, self.check = Fstar, slack, kw, check
+        self.cap = CAP.get(idx, 5000)
+        self.nonconvex = P.c > 0
+
+    def rel(self, F):
+        # certified: (F - F*)/|F*| with F* known to lie in [F_golden - slack, F_golden]
+        return (F - self.Fstar + self.slack) / abs(self.Fstar)
+
+    def run(self, S=None):
+        S = S or self.S
+        updates, launches, kms, sweeps = 0, 0, 0.0, 0
+        st = S.solve(sweeps=self.check, reset=True, **self.kw)
+        stat, reached = None, False
+        while True:
+            updates += st.block_updates
+            launches += st.launches
+            kms += st.kernel_ms
+            sweeps += self.check
+            if self.rel(st.objective) <= TARGET_REL:
+                stat = S.stationarity()
+                launches += 8
+                meas = stat.merit_inf if self.nonconvex else stat.mf_norm2
+                if self.rel(stat.objective) <= TARGET_REL and meas <= TARGET_STAT:
+                    reached = True
+                    break
+            if sweeps >= self.cap:
+                break
+            st = S.solve(sweeps=self.check, **self.kw)
+        if stat is None:
+            stat = S.stationarity()
+        return dict(updates=updates, launches=launches, kernel_ms=kms, sweeps=sweeps, stat=stat,
+                    kernel=st.kernel, delay=st.delay, dobs=st.delay_observed, reached=reached)
+
+
+def measure(args, A, torch, P, idx, stream, local, world, steps, warmup, extra=False):
+    from paper_1701_04900_b200 import asyflexa as _A  # noqa: F401
+    S = A.Solver(P, device=local, mem="device", stream=stream.cuda_stream)
+    sched = A.ASY_SCHED_CYCLIC if args.schedule == "cyclic" else A.ASY_SCHED_RANDOM
+    kw = dict(schedule=sched, seed=1234, workers=args.workers)
+    Fstar, slack = golden_fstar(P, idx)
+    if Fstar is None:
+        raise RuntimeError(f"no oracle F* for configs[{idx}] in tests/golden/fstar_full.json")
+    T = Target(A, S, P, idx, Fstar, slack, kw, args.check_every or CHECK.get(idx, 5))
+    for _ in range(warmup):
+        T.run()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    res = []
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            ev[i][0].record(stream)
+            res.append(T.run())
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    tot_ms = sum(a.elapsed_time(b) for a, b in ev)
+    updates = sum(r["updates"] for r in res)
+    kernel_ms = sum(r["kernel_ms"] for r in res)
+    sweeps = sum(r["sweeps"] for r in res)
+    reached = all(r["reached"] for r in res)
+    tot_ms_all, updates_all = reduce_over_ranks(tot_ms, updates, world, device=f"cuda:{local}")
+    hbm_peak, peak_kind = peaks()
+    achieved = bytes_per_sweep(P) * sweeps / (kernel_ms * 1e-3) / 1e9
+    kname = A.KERNEL_NAMES.get(res[-1]["kernel"], "?")
+    traffic, tsrc = traffic_for(idx, kname)
+    last = res[-1]["stat"]
+    out = {
+        "value": updates_all / (tot_ms_all * 1e-3), "unit": "block_updates/s",
+        "steps": steps, "warmup": warmup,
+        "ms_per_step": tot_ms_all / steps,
+        "time_to_target_ms": (tot_ms_all / steps) if reached else None, "reached": reached,
+        "sweeps_per_step": sweeps / steps, "hbm_gbs": achieved,
+        "workload": workload_name(P, args.schedule),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                     "traffic": None if traffic is None else traffic * T.check, "traffic_source": tsrc,
+                     "kernel": kname, "enforced_delay": res[-1]["delay"],
+                     "observed_delay": res[-1]["dobs"] if res[-1]["dobs"] >= 0 else None,
+                     "algorithmic_bytes_per_launch": bytes_per_sweep(P) * T.check,
+                     "sweeps_per_launch": T.check,
+                     "kernel_ms_per_launch": kernel_ms / max(1, sweeps // T.check)},
+        "final": {"rel_err": (last.objective - Fstar) / abs(Fstar), "Fstar": Fstar, "Fstar_slack": slack,
+                  "mf_norm2": last.mf_norm2, "merit_inf": last.merit_inf,
+                  "stationarity_measure": "merit_inf" if P.c > 0 else "mf_norm2"},
+        "clocks": clk.summary(),
+        "gpu_launches": int(sum(r["launches"] for r in res)),
+    }
+    return out, S, T, kw, Fstar
+
+
 def run_ours(args, rank, world, local):
     import torch
     from paper_1701_04900_b200 import asyflexa as A
@@ -187,146 +310,90 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    P = make_problem(args.config, seed=rank)
     stream = torch.cuda.Stream()
-    S = A.Solver(P, device=local, mem="device", stream=stream.cuda_stream)
-    sched = A.ASY_SCHED_CYCLIC if args.schedule == "cyclic" else A.ASY_SCHED_RANDOM
-    kw = dict(schedule=sched, seed=1234 + rank, panel_rows=args.panel_rows, stages=args.stages,
-              workers=args.workers)
-
-    # F* (untimed): run until the objective stops changing [PAPER.md:434]
-    S.solve(sweeps=50, reset=True, **kw)
-    Fprev = S.objective()
-    for _ in range(200):
-        S.solve(sweeps=25, **kw)
-        F = S.objective()
-        if abs(Fprev - F) <= 1e-15 * abs(F):
-            break
-        Fprev = F
-    st_star = S.stationarity()
-    Fstar = st_star.objective
-
-    def solve_to_target(solver_kw_reset):
-        updates, launches, kms, sweeps = 0, 0, 0.0, 0
-        st = S.solve(sweeps=args.check_every, reset=True, **kw, **solver_kw_reset)
-        while True:
-            updates += st.block_updates
-            launches += st.launches
-            kms += st.kernel_ms
-            sweeps += args.check_every
-            if (st.objective - Fstar) / abs(Fstar) <= TARGET or sweeps >= 5000:
-                break
-            st = S.solve(sweeps=args.check_every, **kw)
-        stat = S.stationarity()
-        return updates, launches + 6, kms, sweeps, stat, st.kernel, st.delay, st.delay_observed
-
-    for _ in range(args.warmup):
-        solve_to_target({})
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    res = []
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            res.append(solve_to_target({}))
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = sum(step_ms)
-    updates = sum(r[0] for r in res)
-    launches = sum(r[1] for r in res)
-    kernel_ms = sum(r[2] for r in res)
-    sweeps = sum(r[3] for r in res)
-    tot_ms_all, updates_all = reduce_over_ranks(tot_ms, updates, world, device=f"cuda:{local}")
-
-    # roofline of the fused async kernel: algorithmic bytes / its device time
-    hbm_peak, peak_kind = peaks()
-    achieved = bytes_per_sweep(P) * sweeps / (kernel_ms * 1e-3) / 1e9
-    traffic = traffic_for(P)
-    if traffic is not None:
-        traffic = traffic * args.check_every  # per launch (one launch = check_every sweeps), like `achieved`
-    last_stat = res[-1][4]
+    P = make_problem(args.config)
+    head, S, T, kw, Fstar = measure(args, A, torch, P, args.config, stream, local, world, args.steps, args.warmup)
+    S.close()
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
         Sh = A.Solver(P, device=local, mem="host", stream=stream.cuda_stream, pinned=True)
-        pstruct = Sh.problem_struct(P)  # pinned host arrays kept alive by Sh
+        pstruct = Sh.pstruct  # page-locked host arrays (registered in place), kept alive by Sh
         xout = torch.empty(P.n, dtype=torch.float64).pin_memory()
+        # A (dense, or CSC colptr + rowidx + vals) + b/y + tau
         h2d = (8 * P.m * P.n if P.kind == "dense" else 12 * P.vals.size + 8 * (P.n + 1)) + 8 * P.m + 8 * P.n
 
         def e2e_step():
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
             A.asy_set_problem(Sh.h, pstruct)
-            u, checks = 0, 0
-            st = Sh.solve(sweeps=args.check_every, reset=True, **kw)
-            while True:
-                u += st.block_updates
-                checks += 1
-                if (st.objective - Fstar) / abs(Fstar) <= TARGET or checks * args.check_every >= 5000:
-                    break
-                st = Sh.solve(sweeps=args.check_every, **kw)
+            t1.record(stream)
+            r = T.run(Sh)
             A.asy_get_x(Sh.h, xout.data_ptr(), A.ASY_MEM_HOST)
-            return u, checks
+            torch.cuda.synchronize()
+            return r, t0.elapsed_time(t1)
 
         e2e_step()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        eu, echecks = 0, 0
-        for _ in range(args.steps):
-            u, c = e2e_step()
-            eu += u
-            echecks += c
+        eu, set_ms = 0, 0.0
+        for _ in range(args.e2e_steps):
+            r, sm = e2e_step()
+            eu += r["updates"]
+            set_ms += sm
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
-        e2e = {"value": eu / (ems * 1e-3), "unit": "block_updates/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * P.n + 8 * echecks / args.steps),
-               "ms_per_step": ems / args.steps}
+        ems_all, eu_all = reduce_over_ranks(ems, eu, world, device=f"cuda:{local}")
+        e2e = {"value": eu_all / (ems_all * 1e-3), "unit": "block_updates/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * P.n + 48),
+               "ms_per_step": ems_all / args.e2e_steps, "steps": args.e2e_steps,
+               "set_problem_ms_per_step": set_ms / args.e2e_steps,
+               "h2d_gbs": h2d / (set_ms / args.e2e_steps * 1e-3) / 1e9}
         Sh.close()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         rate, cores, done, dt = oracle_rate(P, args.cpu_seconds)
         cpu = {"value": rate, "unit": "block_updates/s", "cores": cores, "kind": "oracle",
-               "sample": f"{done} sequential block updates (Algorithm 1, d=0) of the same instance from x0=0, "
+               "sample": f"{done} sequential block updates (Algorithm 1, d=0) of the same instance from x0, "
                          f"{dt:.1f} s, numpy/BLAS fp64"}
+
+    per_config = {}
+    if world == 1 and args.extra:
+        for c in [int(v) for v in args.extra.split(",") if v.strip()]:
+            if c == args.config:
+                continue
+            w, k = next(((w, k) for cc, w, k in EXTRA if cc == c), (2, 3))
+            Pc = make_problem(c)
+            out, Sc, _, _, _ = measure(args, A, torch, Pc, c, stream, local, world, k, w)
+            Sc.close()
+            del Pc
+            per_config[f"configs[{c}]"] = out
 
     if rank == 0:
         line = {
-            "metric": "block updates/sec (async AsyFLEXA) | HBM GB/s vs peak | time to rel. objective err 1e-6",
-            "value": updates_all / (tot_ms_all * 1e-3),
-            "unit": "block_updates/s",
+            "metric": METRIC,
+            "value": head["value"], "unit": "block_updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_ms_all / args.steps,
-            "time_to_rel_err_1e-6_ms": tot_ms_all / args.steps,
-            "sweeps_per_step": sweeps / args.steps,
-            "hbm_gbs": achieved,
+            "ms_per_step": head["ms_per_step"],
+            "time_to_rel_err_1e-6_ms": head["time_to_target_ms"], "reached": head["reached"],
+            "sweeps_per_step": head["sweeps_per_step"], "hbm_gbs": head["hbm_gbs"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded recipe of BASELINE configs, DESIGN.md)",
-            "config": {"workload": workload_name(P, args.schedule), "m": P.m, "n": P.n, "block": P.block,
-                       "gamma": P.gamma, "lambda": P.lam, "check_every_sweeps": args.check_every,
-                       "target_rel_err": TARGET, "parallelism": f"replicas x{world}",
+            "config": {"workload": head["workload"], "m": P.m, "n": P.n, "block": P.block,
+                       "gamma": P.gamma, "lambda": P.lam, "check_every_sweeps": T.check,
+                       "target": f"rel. err <= {TARGET_REL} vs the oracle's F* and stationarity <= {TARGET_STAT}",
+                       "parallelism": f"replicas x{world}",
                        "l2": "inputs larger than L2 (A = %.2f GB vs 126 MB)" % (bytes_per_sweep(P) / 1e9)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "kernel": A.KERNEL_NAMES.get(res[-1][5], "?"),
-                         "enforced_delay": res[-1][6],
-                         "observed_delay": res[-1][7] if res[-1][7] >= 0 else None,
-                         "bytes_per_sweep": bytes_per_sweep(P), "kernel_ms": kernel_ms / args.steps},
-            "final": {"rel_err": (res[-1][4].objective - Fstar) / abs(Fstar), "mf_norm2": last_stat.mf_norm2,
-                      "merit_inf": last_stat.merit_inf, "Fstar": Fstar, "Fstar_mf_norm2": st_star.mf_norm2},
-            "clocks": clk.summary(),
-            "gpu_launches": int(launches),
-            "e2e": e2e,
-            "cpu_baseline": cpu,
+            "roofline": head["roofline"], "final": head["final"], "clocks": head["clocks"],
+            "gpu_launches": head["gpu_launches"],
+            "e2e": e2e, "cpu_baseline": cpu, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
-    S.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -334,7 +401,7 @@ def run_ours(args, rank, world, local):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    P = make_problem(args.config, seed=0)
+    P = make_problem(args.config)
     rate0, cores, _, _ = oracle_rate(P, 2.0)  # warm-up + size the sample
     per_step = max(1.0, min(20.0, 60.0 / max(1, args.steps)))
     for _ in range(args.warmup):
@@ -346,8 +413,7 @@ def run_reference(args, rank, world):
         done_all += done
     tot = time.perf_counter() - t0
     value = done_all / tot
-    line = {"impl": "reference",
-            "metric": "block updates/sec (async AsyFLEXA) | HBM GB/s vs peak | time to rel. objective err 1e-6",
+    line = {"impl": "reference", "metric": METRIC,
             "value": value, "unit": "block_updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -185,6 +185,11 @@ ASY_API int asy_stationarity(asy_handle* h, const double* x, int32_t x_mem,
 /* Copy the current iterate (n entries) to x. */
 ASY_API int asy_get_x(asy_handle* h, double* x, int32_t x_mem);
 
+/* Copy the maintained residual (m entries: LS r = Ax - b, logistic r = Ax, as updated
+ * in place by the block updates -- A_i dx_i pushed into r [PAPER.md:246-260]) to r.  Lets a
+ * caller check it against a fresh Ax - b (rounding drift of the in-place updates). */
+ASY_API int asy_get_residual(asy_handle* h, double* r, int32_t r_mem);
+
 /* F at the current iterate from the maintained residual (no recomputation). */
 ASY_API int asy_objective(asy_handle* h, double* F);
 

@@ -88,6 +88,13 @@ def smooth_value(P, x: np.ndarray) -> float:
     return val - P.c * float(x @ x)
 
 
+def loss_prime(P, z, b):
+    """phi'(z) with grad f = A^T phi'(Ax) - 2c x.  LS: 2s (z - b).  Logistic: -(y/m) sigmoid(-y z)."""
+    if P.loss == "ls":
+        return 2.0 * P.scale * (z - b)
+    return -(b / P.m) * expit(-b * z)
+
+
 def smooth_grad(P, x: np.ndarray) -> np.ndarray:
     """grad f(x) by definition.  LS: 2s A^T(Ax-b) - 2c x.
     Logistic: A^T w - 2c x, w_j = -(y_j/m) sigmoid(-y_j (Ax)_j)."""
@@ -311,17 +318,30 @@ def run_sequential(P, gamma: float, schedule: Iterable[int], x0: Optional[np.nda
     A = design(P)
     x = default_x0(P) if x0 is None else np.array(x0, float)
     z = A @ x
-    lo, hi = lo_hi(P)
     hist = []
     for k, i in enumerate(schedule):
         if refresh_every and k % refresh_every == 0:
             z = A @ x
         j0, j1 = P.block_range(i)
+        if P.kind == "csc":
+            # sparse A_i: the same A_i^T phi'(z) and z += A_i dx over the stored nonzeros only
+            # (phi' evaluated at the rows a column touches; zero entries contribute nothing)
+            grad = np.empty(j1 - j0)
+            for j in range(j0, j1):
+                s, e = P.colptr[j], P.colptr[j + 1]
+                grad[j - j0] = P.vals[s:e] @ loss_prime(P, z[P.rowidx[s:e]], P.b[P.rowidx[s:e]])
+            grad -= 2.0 * P.c * x[j0:j1]
+            xhat = best_response(P, i, x, grad)
+            xnew = x[j0:j1] + gamma * (xhat - x[j0:j1])
+            for j in range(j0, j1):
+                s, e = P.colptr[j], P.colptr[j + 1]
+                z[P.rowidx[s:e]] += P.vals[s:e] * (xnew[j - j0] - x[j])
+            x[j0:j1] = xnew
+            if record_every and (k + 1) % record_every == 0:
+                hist.append((k + 1, objective(P, x)))
+            continue
         Ai = columns(P, j0, j1)
-        if P.loss == "ls":
-            w = 2.0 * P.scale * (z - P.b)
-        else:
-            w = -(P.b / P.m) * expit(-P.b * z)
+        w = loss_prime(P, z, P.b)
         grad = Ai.T @ w - 2.0 * P.c * x[j0:j1]
         xhat = best_response(P, i, x, grad)
         xnew = x[j0:j1] + gamma * (xhat - x[j0:j1])

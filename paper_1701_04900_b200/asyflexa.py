@@ -78,6 +78,7 @@ _lib.asy_solve.argtypes = [_H, C.POINTER(asy_solve_params), C.POINTER(asy_solve_
 _lib.asy_stationarity.argtypes = [_H, _vp, C.c_int32, C.POINTER(asy_stationarity_out)]
 _lib.asy_get_x.argtypes = [_H, _vp, C.c_int32]
 _lib.asy_objective.argtypes = [_H, _dp]
+_lib.asy_get_residual.argtypes = [_H, _vp, C.c_int32]
 _lib.asy_last_error.argtypes = [_H]
 _lib.asy_last_error.restype = C.c_char_p
 _lib.asy_version.restype = C.c_char_p
@@ -136,6 +137,10 @@ def asy_stationarity(h, x_ptr=None, x_mem=ASY_MEM_DEVICE) -> asy_stationarity_ou
 
 def asy_get_x(h, x_ptr, x_mem) -> None:
     _check(_lib.asy_get_x(h, _vp(x_ptr), x_mem), h)
+
+
+def asy_get_residual(h, r_ptr, r_mem) -> None:
+    _check(_lib.asy_get_residual(h, r_ptr, r_mem), h)
 
 
 def asy_objective(h) -> float:
@@ -205,11 +210,12 @@ class Solver:
     def _arr(self, a, dtype):
         a = np.ascontiguousarray(a, dtype=dtype)
         if self.mem == ASY_MEM_HOST:
-            if getattr(self, "_pinned", False):
+            if getattr(self, "_pinned", False) and a.nbytes > 0:
+                # page-lock the array in place (no second host copy of a 32 GB matrix)
                 import torch
-                t = torch.from_numpy(a).pin_memory()
-                self._keep.append(t)
-                return t.data_ptr()
+                rt = torch.cuda.cudart()
+                if int(rt.cudaHostRegister(a.ctypes.data, a.nbytes, 0)) == 0:
+                    self._registered.append(a.ctypes.data)
             self._keep.append(a)
             return a.ctypes.data
         import torch
@@ -249,10 +255,21 @@ class Solver:
         return p
 
     def set_problem(self, P, pinned: bool = False):
+        self._unregister()
         self._keep = []
         self.P = P
         self._pinned = pinned
-        asy_set_problem(self.h, self.problem_struct(P))  # device A / CSC stay borrowed via _keep
+        self.pstruct = self.problem_struct(P)  # host / device arrays kept alive by _keep
+        asy_set_problem(self.h, self.pstruct)  # device A / CSC stay borrowed via _keep
+
+    def _unregister(self):
+        regs = getattr(self, "_registered", [])
+        if regs:
+            import torch
+            rt = torch.cuda.cudart()
+            for ptr in regs:
+                rt.cudaHostUnregister(ptr)
+        self._registered = []
 
     def solve(self, *, mode=ASY_MODE_ASYNC, sweeps=1, gamma=None, schedule=ASY_SCHED_CYCLIC, seed=0,
               max_delay=-1, reset=False, x0=None, f_hist=False, workers=0, panel_rows=0, stages=0):
@@ -280,6 +297,11 @@ class Solver:
     def objective(self) -> float:
         return asy_objective(self.h)
 
+    def residual(self) -> np.ndarray:
+        out = np.zeros(self.P.m)
+        asy_get_residual(self.h, out.ctypes.data, ASY_MEM_HOST)
+        return out
+
     def stationarity(self, x=None) -> asy_stationarity_out:
         if x is None:
             return asy_stationarity(self.h, None, ASY_MEM_DEVICE)
@@ -290,6 +312,7 @@ class Solver:
         if self.h is not None:
             asy_destroy(self.h)
             self.h = None
+        self._unregister()
 
     def __del__(self):
         try:

@@ -149,6 +149,16 @@ static void free_problem(asy_handle* h) {
     h->has_problem = false;
 }
 
+// Before installing a new problem: forget borrowed arrays, KEEP owned device buffers (dev_alloc
+// reuses them when large enough), so re-installing a problem of the same shape -- the e2e path,
+// a new right-hand side -- does no cudaFree / cudaMalloc (each of which synchronises the device).
+static void release_borrowed(asy_handle* h) {
+    Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals};
+    for (Dev* d : all)
+        if (!d->own) *d = Dev{};
+    h->has_problem = false;
+}
+
 static void free_all(asy_handle* h) {
     free_problem(h);
     dev_free(h->red_part);
@@ -351,7 +361,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
         if (p->nnz < 0 || p->nnz >= (int64_t)1 << 31) return h->fail(ASY_ERR_INVALID, "nnz out of range");
     }
     CK(cudaStreamSynchronize(h->stream));
-    free_problem(h);
+    release_borrowed(h);
     const int cm = p->mem;
     h->kind = p->kind;
     h->loss = p->loss;
@@ -365,6 +375,7 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
     if (p->kind == ASY_DENSE_COLMAJOR) {
         const bool aligned = (reinterpret_cast<uintptr_t>(p->A) % 16) == 0 && (p->lda % 2) == 0;
         if (cm == ASY_MEM_DEVICE && aligned) {
+            dev_free(h->A);  // (an owned copy of a previous problem)
             h->A.p = const_cast<double*>(p->A);
             h->A.own = false;
             h->lda = p->lda;
@@ -386,6 +397,9 @@ ASY_API int asy_set_problem(asy_handle* h, const asy_problem* p) {
     } else {
         h->nnz = p->nnz;
         if (cm == ASY_MEM_DEVICE) {
+            dev_free(h->colptr);
+            dev_free(h->rowidx);
+            dev_free(h->vals);
             h->colptr.p = const_cast<int64_t*>(p->colptr);
             h->rowidx.p = const_cast<int32_t*>(p->rowidx);
             h->vals.p = const_cast<double*>(p->vals);
@@ -553,7 +567,7 @@ static EncodeTiledFn encode_tiled() {
 
 struct DenseGeom {
     int64_t R, G, delay;
-    int Bpad, grid, use_tmem;
+    int Bpad, grid, use_tmem, too_tall = 0;
     size_t smem;
     const void* kernel;
 };
@@ -608,6 +622,16 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     const int64_t want = (2 * (delay + 1) * G + kPairs - 1) / kPairs;
     if (want < grid) grid = (int)std::max<int64_t>(1, want);
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
+    // Every panel of a block must be published (handed off) before the block's solve can run, so
+    // the G panels of one block must fit in a quarter of the hand-off rings of the workers
+    // (kRing notes per axpy warp); otherwise a full ring would stall a dot warp that holds its
+    // smem stage while panels of the same block wait for that stage (deadlock).  Such shapes
+    // (very tall blocks on few workers) go to the row-slab kernel instead.
+    if (4 * G > (int64_t)kRing * NAX * grid) {
+        g->too_tall = 1;
+        return h->fail(ASY_ERR_UNSUPPORTED, "panel kernel: %lld panels per block exceed the hand-off capacity of "
+                       "%d workers", (long long)G, grid);
+    }
     // blocks in flight are capped so that a block's panels never fill an axpy warp's hand-off ring
     const int64_t cap = std::max<int64_t>(0, (int64_t)kRing * NAX * grid / (4 * G) - 1);
     g->delay = std::min<int64_t>(delay, cap);
@@ -617,9 +641,13 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
 }
 
 static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
-                              float* ms) {
+                              float* ms, bool* too_tall) {
     DenseGeom geo;
-    TRY(dense_geometry(h, sp, delay, &geo));
+    const int grc = dense_geometry(h, sp, delay, &geo);
+    if (grc != ASY_OK) {
+        if (too_tall) *too_tall = geo.too_tall != 0;
+        return grc;
+    }
     const int64_t B = h->B, R = geo.R, G = geo.G;
     const int Bmax = (int)B;
     EncodeTiledFn enc = encode_tiled();
@@ -1134,8 +1162,13 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
         } else {
             float ms = 0;
             if (h->kind == ASY_DENSE_COLMAJOR) {
-                if (use_slab_kernel(h)) TRY(dense_slab_launch(h, sp, chunk, delay, &ms));
-                else TRY(dense_async_launch(h, sp, chunk, delay, &ms));
+                bool slab = use_slab_kernel(h), too_tall = false;
+                if (!slab) {
+                    const int rc = dense_async_launch(h, sp, chunk, delay, &ms, &too_tall);
+                    if (rc != ASY_OK && !too_tall) return rc;
+                    slab = too_tall;
+                }
+                if (slab) TRY(dense_slab_launch(h, sp, chunk, delay, &ms));
             }
             else TRY(sparse_async_launch(h, sp, chunk, delay, &ms));
             kernel_ms += ms;
@@ -1213,6 +1246,18 @@ ASY_API int asy_get_x(asy_handle* h, double* x, int32_t x_mem) {
     CK(cudaSetDevice(h->device));
     CK(cudaMemcpyAsync(x, h->x.p, sizeof(double) * h->n,
                        x_mem == ASY_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return ASY_OK;
+}
+
+ASY_API int asy_get_residual(asy_handle* h, double* r, int32_t r_mem) {
+    if (!h) return ASY_ERR_INVALID;
+    if (!r) return h->fail(ASY_ERR_INVALID, "r is NULL");
+    if (r_mem != ASY_MEM_HOST && r_mem != ASY_MEM_DEVICE) return h->fail(ASY_ERR_INVALID, "bad r_mem");
+    if (!h->has_problem) return h->fail(ASY_ERR_STATE, "no problem set");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(r, h->r.p, sizeof(double) * h->m,
+                       r_mem == ASY_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     return ASY_OK;
 }

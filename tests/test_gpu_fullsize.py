@@ -1,18 +1,20 @@
 """Full-size parity: BASELINE.json configs[1..4] at their real sizes, in the
 launch configuration bench.py uses.
 
-The oracle cannot run the asynchronous method to convergence at these sizes,
-so the checks are the ones it *can* compute exactly on the host:
   * one synchronous Jacobi sweep (two full GEMVs on the host) -- per-iteration
     parity within 1e-10;
-  * one sequential sweep (Algorithm 1, d = 0) for the dense configs;
-  * at the asynchronous kernel's final iterate: F(x), ||M_F(x)||_2,
-    ||M_F(x)||_inf and the Sec. 4.3 merit recomputed by the oracle from scratch
-    agree with the GPU's stationarity kernel, and the stationarity is below
-    1e-5 (the nonconvex configs[2] uses the merit, reading R11);
-  * configs[1]: the oracle's own F* (sequential run to convergence) is reached
-    within 1e-6.
+  * one sequential sweep (Algorithm 1, d = 0) -- within 1e-10 (configs[4]: 10^6
+    scalar-block updates on both sides);
+  * the asynchronous kernel run to the north_star bar: F within 1e-6 relative of
+    the oracle's F* (tests/golden/fstar_full.json, written by tools/oracle_fstar.py
+    from oracle/ only) and stationarity below 1e-5 (the nonconvex configs[2]: the
+    Sec. 4.3 merit, reading R11); at the final iterate F, ||M_F||_2, ||M_F||_inf
+    recomputed by the oracle agree with the GPU's stationarity kernel, and the
+    maintained residual has not drifted from Ax - b.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -20,6 +22,8 @@ from oracle import asyflexa_oracle as O
 from paper_1701_04900_b200 import inputs
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fstar_full.json")))
 
 
 @pytest.fixture(scope="module")
@@ -48,6 +52,18 @@ def _rel(a, b):
     return abs(a - b) / max(1.0, abs(b))
 
 
+def golden_fstar(P, idx):
+    """(F*, certified slack): the oracle's F* for configs[idx], after checking that the
+    seeded instance is the one the golden was computed on."""
+    g = GOLD[f"config{idx}"]
+    fp = g["fingerprint"]
+    assert (P.m, P.n, P.block, P.gamma) == (fp["m"], fp["n"], fp["block"], fp["gamma"])
+    assert repr(P.lam) == fp["lam"] and repr(float(P.b.sum())) == fp["b_sum"]
+    assert repr(float(P.tau.sum())) == fp["tau_sum"]
+    # configs[4]: F* is certified only to [F - gap, F] (duality gap of the candidate)
+    return float(g["F_star"]), float(g.get("duality_gap", 0.0)) if idx == 4 else 0.0
+
+
 @pytest.mark.parametrize("idx", [1, 2, 3, 4])
 def test_fullsize_jacobi_sweep(A, idx):
     P = problem(idx)
@@ -61,7 +77,7 @@ def test_fullsize_jacobi_sweep(A, idx):
         S.close()
 
 
-@pytest.mark.parametrize("idx", [1, 2, 3])
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
 def test_fullsize_sequential_sweep(A, idx):
     P = problem(idx)
     S = A.Solver(P)
@@ -69,36 +85,46 @@ def test_fullsize_sequential_sweep(A, idx):
         S.solve(sweeps=1, reset=True, max_delay=0)
         x_or, _ = O.run_sequential(P, P.gamma, range(P.nblocks))
         assert _rel_x(S.x(), x_or) <= 1e-10
+        assert _rel(S.objective(), O.objective(P, x_or)) <= 1e-10
     finally:
         S.close()
 
 
-BUDGET = {1: (100, 10), 2: (4000, 500), 3: (200, 10), 4: (2000, 250)}
+# (sweeps budget, sweeps per check): configs[4] needs ~3e4 sweeps to 1e-6 (the l1-logistic
+# instance itself: synchronous Jacobi needs as many), ~9 s of kernel time
+BUDGET = {1: (200, 5), 2: (4000, 100), 3: (200, 5), 4: (80000, 2000)}
 
 
 @pytest.mark.parametrize("idx", [1, 2, 3, 4])
-def test_fullsize_async_stationary(A, idx):
+def test_fullsize_async_reaches_oracle_fstar(A, idx):
     P = problem(idx)
+    F_star, slack = golden_fstar(P, idx)
     S = A.Solver(P)
     total, chunk = BUDGET[idx]
     try:
         S.solve(sweeps=0, reset=True)
-        done = 0
+        done, ok = 0, False
         while done < total:
-            S.solve(sweeps=chunk)
+            st = S.solve(sweeps=chunk)
             done += chunk
+            if (st.objective - F_star) / abs(F_star) > 1e-6 - slack / abs(F_star):
+                continue
             out = S.stationarity()
             meas = out.merit_inf if idx == 2 else out.mf_norm2
-            if meas <= 1e-6:
+            if (out.objective - F_star) / abs(F_star) <= 1e-6 - slack / abs(F_star) and meas <= 1e-5:
+                ok = True
                 break
+        assert ok, (idx, done, st.objective, F_star)
+        # F below the oracle's F* by more than rounding would mean F* is not the minimum
+        assert (out.objective - F_star) / abs(F_star) >= -1e-12 - slack / abs(F_star)
         x = S.x()
         mf = O.stationarity(P, x)
         assert _rel(out.objective, O.objective(P, x)) <= 1e-9
         assert abs(out.mf_norm2 - np.linalg.norm(mf)) <= 1e-6 * max(1.0, np.linalg.norm(mf)) + 1e-12
         assert abs(out.mf_norminf - np.abs(mf).max()) <= 1e-6 * max(1.0, np.abs(mf).max()) + 1e-12
-        assert meas <= 1e-5, (idx, meas)
-        if idx == 1:
-            _, F_star, _ = O.estimate_fstar(P, P.gamma, max_sweeps=200, tol=1e-15)
-            assert _rel(out.objective, F_star) <= 1e-6
+        z = O.design(P) @ x
+        fresh = z - P.b if P.loss == "ls" else z
+        assert float(np.max(np.abs(S.residual() - fresh))) <= 1e-10 * max(1.0, float(np.max(np.abs(fresh))))
+        assert 0 <= st.delay and (st.delay_observed < 0 or st.delay_observed <= st.delay)
     finally:
         S.close()

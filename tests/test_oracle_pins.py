@@ -419,3 +419,21 @@ def test_liblinear_candidate_is_certified():
     xs, Fs, _ = O.estimate_fstar(Q, 1.0, max_sweeps=100000, tol=0.0)
     assert O.duality_gap_l1(Q, x) <= 1e-7 * O.objective(Q, x)
     assert abs(O.objective(Q, x) - Fs) <= 1e-8 * abs(Fs)
+
+
+@pytest.mark.parametrize("loss", ["logistic", "ls"])
+def test_sparse_column_path_equals_dense(loss):
+    """run_sequential on a CSC matrix (per-column nonzeros) == the same run on its dense copy
+    (A_i^T phi'(z) and z += A_i dx of Algorithm 1 [PAPER.md:246-260]), blocks of 1 and 3."""
+    for block in (1, 3):
+        Q = inputs.sparse_logistic(40, 30, density=0.15, seed=9, lam_frac=0.05)
+        if loss == "ls":
+            Q.loss, Q.scale, Q.b = "ls", 0.5, np.random.default_rng(2).normal(size=Q.m)
+            Q.tau = np.sum(inputs.csc_to_dense(Q) ** 2, axis=0) + 1e-3
+        Q.block = block
+        D = inputs.Problem(**{**Q.__dict__, "kind": "dense", "A": inputs.csc_to_dense(Q)})
+        sched = list(O.cyclic_schedule(Q.nblocks, 5))
+        xs, hs = O.run_sequential(Q, 0.9, sched, record_every=Q.nblocks)
+        xd, hd = O.run_sequential(D, 0.9, sched, record_every=Q.nblocks)
+        np.testing.assert_allclose(xs, xd, rtol=0, atol=1e-13)
+        np.testing.assert_allclose([h[1] for h in hs], [h[1] for h in hd], rtol=1e-13)

@@ -1,5 +1,6 @@
 """Multi-process host logic of the replica benchmark (world size 2, gloo, CPU):
-max-over-ranks time, sum-over-ranks work, distinct per-rank instances."""
+max-over-ranks time, sum-over-ranks work, every rank solving the same seeded instance
+(so the oracle's F* golden is every replica's target)."""
 import os
 import socket
 
@@ -22,8 +23,8 @@ def _worker(rank, world, port, out):
     import bench
     from paper_1701_04900_b200 import inputs
     ms, units = bench.reduce_over_ranks(10.0 + 5 * rank, 100.0 * (rank + 1), world, device="cpu")
-    P = bench.make_problem(0, seed=rank)
-    out[rank] = (ms, units, float(P.b[:5].sum()))
+    P = bench.make_problem(0)
+    out[rank] = (ms, units, float(P.b.sum()), P.meta["config_idx"])
     dist.barrier()
     dist.destroy_process_group()
 
@@ -36,6 +37,6 @@ def test_replica_reduction_gloo():
         mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
         res = dict(out)
     for r in range(world):
-        ms, units, _ = res[r]
-        assert ms == 15.0 and units == 300.0
-    assert res[0][2] != res[1][2]  # replicas solve different seeded instances
+        ms, units, _, idx = res[r]
+        assert ms == 15.0 and units == 300.0 and idx == 0
+    assert res[0][2] == res[1][2]  # replicas solve the same seeded instance
