@@ -1,4 +1,4 @@
-"""Write tests/golden/fstar_full.json: the oracle's F* for BASELINE configs[1..4] at full size.
+"""Write tests/golden/fstar_full.json: the oracle's F* for BASELINE configs[0..4] at full size.
 
 Calls only oracle/ (and the seeded input recipe).  F* follows the paper: "run ... until
 variations in the objective value were undetectable" [PAPER.md:434] -- the oracle's
@@ -35,7 +35,7 @@ def run(idx):
     P = inputs.config(idx)
     rec = {"fingerprint": fingerprint(P), "gen_s": time.time() - t0}
     t1 = time.time()
-    if idx in (1, 2, 3):
+    if idx in (0, 1, 2, 3):
         x, F, sweeps = O.estimate_fstar(P, P.gamma, max_sweeps=20000, tol=1e-15)
         rec.update(method="oracle Algorithm 1 (d=0, cyclic) until |dF| <= 1e-15 |F| per sweep [PAPER.md:434]",
                    sweeps=sweeps, converged=sweeps < 20000)
