@@ -1085,25 +1085,36 @@ static bool use_slab_kernel(const asy_handle* h) {
     return per_sm >= 64.0 * 1024.0;
 }
 
+#ifndef ASY_SPARSE_LPC
+#define ASY_SPARSE_LPC 2  // lanes per column of the CSC kernel (16 block updates in flight per warp)
+#endif
 static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
                                float* ms) {
+    constexpr int LPC = ASY_SPARSE_LPC;
     void (*kern)(SparseAsyncParams) =
-        h->S.loss == LOSS_LS ? sparse_async_kernel<LOSS_LS> : sparse_async_kernel<LOSS_LOGISTIC>;
+        h->S.loss == LOSS_LS ? sparse_async_kernel<LOSS_LS, LPC> : sparse_async_kernel<LOSS_LOGISTIC, LPC>;
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, kSparseThreads, 0));
     int grid = std::max(1, occ) * h->sms;
     if (sp->workers > 0) grid = std::min(grid, (int)sp->workers);
-    const int64_t slots = next_pow2(std::max<int64_t>(1 << 20, 2 * (delay + 2)));
+    // batch size: 32 / LPC updates per warp, at most delay + 1 (a batch never waits for itself)
+    const int BS = (int)std::min<int64_t>(32 / LPC, delay + 1);
+    const int64_t NB = (h->n + BS - 1) / BS;
+    const int64_t warps = (int64_t)grid * (kSparseThreads / 32);
+    const int64_t slots = next_pow2(std::max<int64_t>(1024, delay / BS + 4 * warps + 64));
     TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->n));
     TRY(dev_alloc(h, h->rs, sizeof(double) * 2 * h->m));  // [r_i, aux_i] pairs for the launch
+    TRY(dev_alloc(h, h->dobs, sizeof(unsigned)));
     SparseAsyncParams P{};
     P.colptr = P_<int64_t>(h->colptr); P.rowidx = P_<int32_t>(h->rowidx); P.vals = P_<double>(h->vals);
-    P.m = h->m; P.n = h->n; P.r = P_<double>(h->rs); P.aux = P_<double>(h->b); P.x = P_<double>(h->x);
+    P.m = h->m; P.n = h->n; P.r = P_<double>(h->rs); P.x = P_<double>(h->x);
     P.tau = P_<double>(h->tau); P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed;
-    P.epoch0 = h->epochs; P.K = sweeps * h->n; P.delay = delay; P.counter = P_<unsigned long long>(h->counter);
+    P.epoch0 = h->epochs; P.T = sweeps * NB; P.NB = NB; P.BS = BS; P.delay = delay;
+    P.counter = P_<unsigned long long>(h->counter);
+    P.gwm = P_<unsigned long long>(h->counter) + 4;  // (another 32-byte sector of the counter line)
     P.ver = P_<unsigned>(h->ver); P.done = P_<long long>(h->done); P.slots = slots;
-    P.chunk = delay == 0 ? 4 : 32;
+    P.dobs = P_<unsigned>(h->dobs);
     h->last_kernel = ASY_KERNEL_SPARSE;
     h->last_delay = (int)delay;
     sparse_async_init<<<grid_for(std::max<int64_t>(slots, h->n), 256, 8 * h->sms), 256, 0, h->stream>>>(P);
@@ -1120,6 +1131,11 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    {
+        unsigned dobs = 0;
+        CK(cudaMemcpy(&dobs, h->dobs.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        h->last_dobs = std::max(h->last_dobs, (int)dobs);
+    }
     return ASY_OK;
 }
 

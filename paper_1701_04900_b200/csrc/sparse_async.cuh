@@ -1,14 +1,32 @@
 // sparse_async.cuh -- asynchronous scalar-block updates on a CSC matrix.
 //
-// Algorithm 1 [PAPER.md:246-260] with N = n scalar blocks (the paper's own
-// setting, "always setting N=n" [PAPER.md:382]).  Persistent warps claim
-// chunks of sequence numbers from one global atomic counter; each 8-lane
-// group of a warp performs one block update at a time: gather the column's
-// nonzeros, read the shared residual at those rows (inconsistent read),
-// phi'(r) . a_j with a shuffle reduction, closed-form best response (Eq. 2),
-// (S.4) on x_j, and scatter a_j * dx_j back into r with atomicAdd.
-// Guards: D4 freshness (ver[j] = number of applied updates of column j) and
-// the bounded-delay window D1 (done[] ring), both pointing to older sequences.
+// Algorithm 1 [PAPER.md:246-260] with N = n scalar blocks (the paper's own setting,
+// "always setting N=n" [PAPER.md:382]).  Persistent warps are the asynchronous workers.
+// Work is handed out in BATCHES of BS consecutive sequence numbers of one epoch (a batch
+// never crosses an epoch boundary, so it never holds the same block twice): batch t is
+// epoch e = t / NB, positions [i0, i0 + BS) with i0 = (t mod NB) BS, NB = ceil(N / BS).
+// Each batch is claimed by one warp from a global atomic counter; LPC lanes per column,
+// so BS = 32 / LPC block updates are in flight per warp at once (the update's chain is a
+// few dependent L2 round trips -- colptr, row indices, the residual gathers -- so the
+// warp keeps many independent chains in flight instead of one).  Per update: gather the
+// column's nonzeros, read the shared residual at those rows (inconsistent read),
+// phi'(r) . a_j, the closed-form best response (Eq. 2), (S.4) on x_j, and scatter
+// a_j dx_j back into r with red.add.
+//
+// Guards (checked for the whole batch before it reads; all point to strictly older
+// batches, so co-resident warps cannot deadlock):
+//   * bounded delay D1 [PAPER.md:224] with an in-order watermark: `gwm` is the number of
+//     leading batches that are complete; batch t reads only when every sequence up to
+//     k_max(t) - delta - 1 is complete, i.e. gwm > batch(k_max - delta - 1).  BS <= delta + 1
+//     keeps that batch strictly older than t.  The warp that completes batch t marks
+//     done[t mod S] = t and, if gwm == t, advances gwm over t and every later batch already
+//     marked (a fence.sc between the mark and the watermark read on both sides, so two
+//     warps finishing adjacent batches cannot both miss each other);
+//   * own-block freshness D4 [PAPER.md:233]: ver[j] = number of applied updates of block j;
+//     the update of epoch e waits for ver[j] >= e.
+// delta == 0 gives BS = 1 and the sequential (d^k = 0) scheme, bit-reproducible.
+// Observed delay: the largest k - k_first(gwm) over the batch's sequences at read time (an
+// upper bound on d^k of Assumption D1: every update before batch gwm was applied).
 #pragma once
 #include "common.cuh"
 
@@ -20,7 +38,6 @@ struct SparseAsyncParams {
     const double* __restrict__ vals;
     int64_t m, n;
     double* r;         // the residual's pair buffer [r_i, aux_i] (2 m doubles; r_i at 2 i)
-    const double* aux; // (unused by the kernel: aux_i is at r[2 i + 1])
     double* x;
     const double* tau;
     Scalars S;
@@ -28,13 +45,16 @@ struct SparseAsyncParams {
     int sched;
     uint64_t seed;
     int64_t epoch0;
-    int64_t K;        // block updates in this launch
+    int64_t T;        // batches in this launch = sweeps * NB
+    int64_t NB;       // batches per epoch
+    int BS;           // block updates per batch (<= 32 / LPC, <= delay + 1)
     int64_t delay;
-    unsigned long long* counter;
-    unsigned* ver;    // [n]
-    long long* done;  // [slots]
-    int64_t slots;
-    int chunk;
+    unsigned long long* counter;  // batch claims
+    unsigned long long* gwm;      // in-order completion watermark (batches)
+    unsigned* ver;                // [n]
+    long long* done;              // [S] done[t mod S] = t once batch t is complete
+    int64_t slots;                // S, power of two
+    unsigned* dobs;               // observed delay (max)
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32_g(const unsigned* p) {
@@ -47,26 +67,24 @@ __device__ __forceinline__ long long ld_relaxed_s64_g(const long long* p) {
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void red_relaxed_max_s64_g(long long* p, long long v) {
-    asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64_g(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_s64_g(long long* p, long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_relaxed_u32_g(unsigned* p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// relaxed polls (an acquire per poll would invalidate the SM's L1); the caller fences once
-__device__ __forceinline__ void spin_relaxed_u32_g(const unsigned* p, unsigned v) {
-    unsigned ns = 32;
-    while (ld_relaxed_u32_g(p) < v) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-    }
+__device__ __forceinline__ void red_relaxed_add_f64_g(double* p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
-__device__ __forceinline__ void spin_relaxed_s64_g(const long long* p, long long v) {
-    unsigned ns = 32;
-    while (ld_relaxed_s64_g(p) < v) {
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-    }
+__device__ __forceinline__ double2 ld_relaxed_f64x2(const double* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
 }
 
 // residual and b / y interleaved for the launch (one 16-byte gather per nonzero), and back
@@ -80,169 +98,218 @@ __global__ void sparse_pair_unpack(const double* ry, double* r, int64_t m) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
         r[i] = ry[2 * i];
 }
-__device__ __forceinline__ double2 ld_relaxed_f64x2(const double* p) {
-    double2 v;
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-    return v;
-}
 
 __global__ void sparse_async_init(SparseAsyncParams P) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    if (tid == 0) *P.counter = 0ull;
-    for (int64_t s = tid; s < P.slots; s += nth) P.done[s] = (long long)s - (long long)P.slots;
+    if (tid == 0) {
+        *P.counter = 0ull;
+        *P.gwm = 0ull;
+        *P.dobs = 0u;
+    }
+    for (int64_t s = tid; s < P.slots; s += nth) P.done[s] = -1;
     for (int64_t j = tid; j < P.n; j += nth) P.ver[j] = 0u;
 }
 
-// One block update's dependency chain is a few L2 round trips, so the kernel is arranged
-// to issue independent loads together: the guard loads, colptr, and (after colptr) the
-// column's row indices / values and x_j, tau_j are in flight at once; the residual is
-// gathered only after the guards passed.  No 64-bit division per update (the epoch and
-// position advance incrementally), one fence per update (after the scatter, before the
-// version / window counters; deferred to overlap the next update's loads), no returning
-// atomics on the path, the loss fixed at compile time.
-#ifndef ASY_SPARSE_MINB
-#define ASY_SPARSE_MINB 1
-#endif
 #ifndef ASY_SPARSE_THREADS
-#define ASY_SPARSE_THREADS 128  // small CTAs: finer occupancy granularity at ~87 registers
+#define ASY_SPARSE_THREADS 128
+#endif
+#ifndef ASY_SPARSE_CH
+#define ASY_SPARSE_CH 8  // nonzeros per lane held in registers (longer columns loop over the rest)
 #endif
 constexpr int kSparseThreads = ASY_SPARSE_THREADS;
-template <int LOSS>
-__global__ void __launch_bounds__(kSparseThreads, ASY_SPARSE_MINB) sparse_async_kernel(SparseAsyncParams P) {
+constexpr int kSparseCh = ASY_SPARSE_CH;
+
+// LPC lanes per column (1, 2, 4 or 8): batch lanes b = lane / LPC, element lane e = lane % LPC.
+template <int LOSS, int LPC>
+__global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
-    const int grp = lane >> 3, gl = lane & 7;
-    const unsigned gmask = 0xFFu << (grp * 8);
-    const int64_t N = P.n;
+    const int bl = lane / LPC, el = lane % LPC;
+    const unsigned cmask = LPC == 32 ? 0xffffffffu : (((1u << LPC) - 1u) << (bl * LPC));
+    const int64_t N = P.n, NB = P.NB;
+    const int BS = P.BS;
     const int half = perm_half_bits(N);
+    const int64_t S = P.slots;
     PermKeys pk{};
     int64_t pkE = -1;
-    // completion of the group's previous update (fence, then its version and window counters),
-    // issued once the next update's first loads are in flight; never deferred across a wait
-    bool pend = false;
-    int64_t pj = 0;
-    long long pkk = 0;
-    auto flush = [&]() {
-        if (pend && gl == 0) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // its scatter and x_j first
-            red_relaxed_u32_g(&P.ver[pj], 1u);
-            red_relaxed_max_s64_g(&P.done[pkk & (P.slots - 1)], pkk);  // monotone window counter
-        }
-        pend = false;
+    unsigned dmax = 0;
+
+    // the head of a batch's update for this lane: sequence, block, column extent, x / tau / ver
+    struct Head {
+        long long t;      // batch (-1: none)
+        int64_t e, k, j;  // epoch (local), sequence (local), block = column
+        int64_t s, c;     // column start, nonzero count
+        bool live;        // this lane's update exists
+        unsigned vj;
+        double tj;
     };
-    for (;;) {
-        long long base = 0;
-        if (lane == 0) base = (long long)atomicAdd(P.counter, (unsigned long long)P.chunk);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= P.K) break;
-        const long long kend = (base + P.chunk) < P.K ? (base + P.chunk) : P.K;
-        // local epoch u and position i of this group's first sequence (one division per chunk)
-        long long k = base + grp;
-        int64_t u = k / N, i = k - u * N;
-        // the head of an update: its column (S.1), guard counters and column extent; the
-        // next update's head is loaded while the current one runs (counters are monotone, so an
-        // early read can only be stale-low: the guard then re-polls)
-        struct Head { int64_t j, s, e; unsigned vj; long long dn; };
-        auto head = [&](long long kk, int64_t ii, int64_t uu) {
-            Head hd;
-            hd.j = ii;
+    auto head = [&](long long t) {
+        Head h;
+        h.t = t;
+        h.e = t / NB;
+        const int64_t i0 = (t - h.e * NB) * (int64_t)BS;
+        const int64_t i = i0 + bl;
+        h.live = t < P.T && bl < BS && i < N;
+        h.k = h.e * N + i;
+        h.j = 0; h.s = 0; h.c = 0; h.vj = 0; h.tj = 1.0;
+        if (h.live) {
+            h.j = i;
             if (P.sched == SCHED_RANDOM) {
-                const int64_t E = P.epoch0 + uu;
+                const int64_t E = P.epoch0 + h.e;
                 if (E != pkE) { pk = perm_keys(P.seed, E); pkE = E; }
-                uint64_t v = (uint64_t)ii;
+                uint64_t v = (uint64_t)i;
                 do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
-                hd.j = (int64_t)v;
+                h.j = (int64_t)v;
             }
-            const long long kd = kk - P.delay - 1;
-            hd.vj = 0;
-            hd.dn = 0;
-            if (gl == 0) {
-                hd.vj = ld_relaxed_u32_g(&P.ver[hd.j]);
-                if (kd >= 0) hd.dn = ld_relaxed_s64_g(&P.done[kd & (P.slots - 1)]);
+            h.s = __ldg(&P.colptr[h.j]);
+            h.c = __ldg(&P.colptr[h.j + 1]) - h.s;
+            if (el == 0) {
+                h.vj = ld_relaxed_u32_g(&P.ver[h.j]);
+                h.tj = __ldg(&P.tau[h.j]);
             }
-            hd.s = __ldg(&P.colptr[hd.j]);
-            hd.e = __ldg(&P.colptr[hd.j + 1]);
-            return hd;
-        };
-        Head nx{};
-        if (k < kend) nx = head(k, i, u);
-        for (; k < kend; k += 4) {
-            const Head cur = nx;
-            const int64_t j = cur.j, s = cur.s, e = cur.e;
-            const long long kd = k - P.delay - 1;
-            const unsigned vj = cur.vj;
-            const long long dn = cur.dn;
-            // this lane's first two nonzeros (columns of up to 16 in one round trip; ~10 on
-            // average in configs[4]) and the block's x / tau (x_j final once ver[j] == u)
-            int32_t row0 = 0, row1 = 0;
-            double val0 = 0.0, val1 = 0.0;
-            if (s + gl < e) {
-                row0 = __ldg(&P.rowidx[s + gl]);
-                val0 = __ldg(&P.vals[s + gl]);
+        }
+        return h;
+    };
+    auto claim = [&]() {
+        long long t = 0;
+        if (lane == 0) t = (long long)atomicAdd(P.counter, 1ull);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    auto kfirst = [&](long long t) { const int64_t e = t / NB; return e * N + (t - e * NB) * (int64_t)BS; };
+    // batch containing sequence k (local numbering)
+    auto batch_of = [&](long long k) { const int64_t e = k / N; return e * NB + (k - e * N) / BS; };
+
+    // completion of batch t (after its scatter): fence (the batch's r red.adds and x stores
+    // first), per-block versions, the batch mark, and the in-order watermark advance
+    long long pend = -1;
+    int64_t pend_j = 0;
+    bool pend_live = false;
+    auto complete = [&]() {
+        if (pend < 0) return;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // every lane: its own atomics / x store
+        if (pend_live && el == 0) red_relaxed_u32_g(&P.ver[pend_j], 1u);
+        __syncwarp();
+        if (lane == 0) {
+            st_relaxed_s64_g(&P.done[pend & (S - 1)], pend);
+            asm volatile("fence.sc.gpu;" ::: "memory");
+            unsigned long long t = (unsigned long long)pend;
+            for (;;) {
+                if (atomicCAS(P.gwm, t, t + 1) != t) break;  // an older batch is still running
+                ++t;
+                asm volatile("fence.sc.gpu;" ::: "memory");
+                if (ld_relaxed_s64_g(&P.done[t & (S - 1)]) != (long long)t) break;
             }
-            if (s + gl + 8 < e) {
-                row1 = __ldg(&P.rowidx[s + gl + 8]);
-                val1 = __ldg(&P.vals[s + gl + 8]);
-            }
-            const int64_t ucur = u;
-            i += 4;
-            while (i >= N) { i -= N; ++u; }
-            if (k + 4 < kend) nx = head(k + 4, i, u);
-            double tj = 0.0;
-            if (gl == 0) {
-                tj = __ldg(&P.tau[j]);
-                const bool ok4 = vj >= (unsigned)ucur, ok1 = kd < 0 || dn >= kd;
-                if (!ok4 || !ok1) {
-                    flush();  // (the awaited update may be this group's pending one)
-                    if (!ok4) spin_relaxed_u32_g(&P.ver[j], (unsigned)ucur);                   // D4
-                    if (!ok1) spin_relaxed_s64_g(&P.done[kd & (P.slots - 1)], kd);             // D1
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+        pend = -1;
+    };
+
+    long long t = claim();
+    Head nx = head(t);
+    while (nx.t < P.T) {
+        const Head cur = nx;
+        // previous batch's completion (its fence also waits for this head's loads)
+        complete();
+        // D1: every sequence up to k_max - delta - 1 complete (in-order watermark)
+        {
+            const int64_t i0 = (cur.t - cur.e * NB) * (int64_t)BS;
+            const int64_t nlive = (N - i0) < BS ? (N - i0) : BS;
+            const long long kmax = cur.e * N + i0 + nlive - 1;
+            const long long kd = kmax - P.delay - 1;
+            unsigned long long w = 0;
+            if (lane == 0) {
+                w = ld_relaxed_u64_g(P.gwm);
+                if (kd >= 0) {
+                    const unsigned long long need = (unsigned long long)batch_of(kd) + 1ull;
+                    unsigned ns = 32;
+                    while (w < need) {
+                        __nanosleep(ns);
+                        if (ns < 256) ns <<= 1;
+                        w = ld_relaxed_u64_g(P.gwm);
+                    }
                 }
             }
-            flush();
-            __syncwarp(gmask);
+            w = __shfl_sync(0xffffffffu, w, 0);
+            // observed delay: sequences before batch w are all applied
+            if (cur.live && el == 0) {
+                const long long miss = cur.k - kfirst((long long)w);
+                if (miss > (long long)dmax) dmax = (unsigned)miss;
+            }
+        }
+        // D4: the previous update of this block applied
+        if (cur.live && el == 0 && cur.vj < (unsigned)cur.e) {
+            unsigned ns = 32;
+            while (ld_relaxed_u32_g(&P.ver[cur.j]) < (unsigned)cur.e) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+        __syncwarp();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire (every lane observed a guard)
+        // next batch: claim and load its head while this one runs
+        const long long tn = claim();
+        nx = head(tn);
+        if (cur.live) {
             double xj = 0.0;
-            if (gl == 0) xj = ld_relaxed_f64(&P.x[j]);
+            if (el == 0) xj = ld_relaxed_f64(&P.x[cur.j]);
             // gradient: sum_q a_qj phi'(r_q) over the column (inconsistent read of r)
+            int32_t rows[kSparseCh];
+            double vv[kSparseCh];
+#pragma unroll
+            for (int u = 0; u < kSparseCh; ++u) {
+                const int64_t q = el + (int64_t)u * LPC;
+                rows[u] = 0;
+                vv[u] = 0.0;
+                if (q < cur.c) {
+                    rows[u] = __ldg(&P.rowidx[cur.s + q]);
+                    vv[u] = __ldg(&P.vals[cur.s + q]);
+                }
+            }
             double acc = 0.0;
-            {
-                double2 ra0 = make_double2(0.0, 0.0), ra1 = make_double2(0.0, 0.0);
-                if (s + gl < e) ra0 = ld_relaxed_f64x2(&P.r[2 * (int64_t)row0]);
-                if (s + gl + 8 < e) ra1 = ld_relaxed_f64x2(&P.r[2 * (int64_t)row1]);
-                if (s + gl < e) acc = val0 * loss_prime_t<LOSS>(P.S, ra0.x, ra0.y);
-                if (s + gl + 8 < e) acc = fma(val1, loss_prime_t<LOSS>(P.S, ra1.x, ra1.y), acc);
+#pragma unroll
+            for (int u = 0; u < kSparseCh; ++u) {
+                const int64_t q = el + (int64_t)u * LPC;
+                if (q < cur.c) {
+                    const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)rows[u]]);
+                    acc = fma(vv[u], loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
+                }
             }
-            for (int64_t q = s + gl + 16; q < e; q += 8) {
-                const int32_t row = __ldg(&P.rowidx[q]);
+            for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cur.c; q += LPC) {
+                const int32_t row = __ldg(&P.rowidx[cur.s + q]);
                 const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)row]);
-                acc = fma(__ldg(&P.vals[q]), loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
+                acc = fma(__ldg(&P.vals[cur.s + q]), loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
             }
-            acc += __shfl_xor_sync(gmask, acc, 4);
-            acc += __shfl_xor_sync(gmask, acc, 2);
-            acc += __shfl_xor_sync(gmask, acc, 1);
+#pragma unroll
+            for (int o = LPC / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(cmask, acc, o);
             double d = 0.0;
-            if (gl == 0) {
-                const double xh = best_response(P.S, acc, xj, tj, j);
+            if (el == 0) {
+                const double xh = best_response(P.S, acc, xj, cur.tj, cur.j);
                 const double xn = xj + P.gamma * (xh - xj);
-                P.x[j] = xn;
+                P.x[cur.j] = xn;
                 d = xn - xj;
             }
-            d = __shfl_sync(gmask, d, grp * 8);
+            if (LPC > 1) d = __shfl_sync(cmask, d, bl * LPC);
             if (d != 0.0) {
-                if (s + gl < e) atomicAdd(&P.r[2 * (int64_t)row0], val0 * d);
-                if (s + gl + 8 < e) atomicAdd(&P.r[2 * (int64_t)row1], val1 * d);
-                for (int64_t q = s + gl + 16; q < e; q += 8)
-                    atomicAdd(&P.r[2 * (int64_t)__ldg(&P.rowidx[q])], __ldg(&P.vals[q]) * d);
+#pragma unroll
+                for (int u = 0; u < kSparseCh; ++u) {
+                    const int64_t q = el + (int64_t)u * LPC;
+                    if (q < cur.c) red_relaxed_add_f64_g(&P.r[2 * (int64_t)rows[u]], vv[u] * d);
+                }
+                for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cur.c; q += LPC)
+                    red_relaxed_add_f64_g(&P.r[2 * (int64_t)__ldg(&P.rowidx[cur.s + q])], __ldg(&P.vals[cur.s + q]) * d);
             }
-            __syncwarp(gmask);  // (orders the group's atomics before lane 0's later fence)
-            pend = true;
-            pj = j;
-            pkk = k;
         }
-        // before the warp-wide claim: another group of this warp may be waiting for it
-        flush();
-        __syncwarp();
+        pend = cur.t;
+        pend_j = cur.j;
+        pend_live = cur.live;
     }
+    complete();
+    // warp max of the observed delay, one atomic per warp
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned v = __shfl_xor_sync(0xffffffffu, dmax, o);
+        dmax = v > dmax ? v : dmax;
+    }
+    if (lane == 0 && dmax > 0) atomicMax(P.dobs, dmax);
 }
 
 }  // namespace asy

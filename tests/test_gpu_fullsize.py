@@ -58,8 +58,10 @@ def golden_fstar(P, idx):
     g = GOLD[f"config{idx}"]
     fp = g["fingerprint"]
     assert (P.m, P.n, P.block, P.gamma) == (fp["m"], fp["n"], fp["block"], fp["gamma"])
-    assert repr(P.lam) == fp["lam"] and repr(float(P.b.sum())) == fp["b_sum"]
-    assert repr(float(P.tau.sum())) == fp["tau_sum"]
+    # (b = A x* + e goes through a host BLAS GEMV: bit-identical instances are not guaranteed
+    # across machines, ulp-level differences are -- they move F* by ~1e-16 relative)
+    for v, key in ((P.lam, "lam"), (float(P.b.sum()), "b_sum"), (float(P.tau.sum()), "tau_sum")):
+        assert abs(v - float(fp[key])) <= 1e-12 * max(1.0, abs(float(fp[key]))), (key, v, fp[key])
     # configs[4]: F* is certified only to [F - gap, F] (duality gap of the candidate)
     return float(g["F_star"]), float(g.get("duality_gap", 0.0)) if idx == 4 else 0.0
 
