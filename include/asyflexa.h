@@ -119,6 +119,20 @@ typedef struct {
     int64_t block_size;
 } asy_problem;
 
+/* Kernel choice and geometry overrides of the dense asynchronous kernels, for tests and
+ * measurements (every field 0 = automatic; NULL pointer = all automatic).  None changes the
+ * arithmetic: every variant computes the same Algorithm 1 updates (Kernels). */
+typedef struct {
+    int32_t dense_kernel;    /* 0 auto | ASY_KERNEL_DENSE_PANEL | ASY_KERNEL_DENSE_SLAB_TMEM (row-slab family:
+                                the TMEM form when its park ring fits, else the smem/L2 form) |
+                                ASY_KERNEL_DENSE_SLAB (the smem/L2 row-slab form) */
+    int32_t panel_park;      /* panel kernel: 0 park panels in TMEM, 2 never (re-read them from L2) */
+    int32_t slab_hold;       /* smem/L2 slab form: 0 auto, 1 hold the chunks in smem, 2 re-load them from L2 */
+    int32_t slab_chunk_rows; /* smem/L2 slab form: rows per chunk (even, <= 256; 0 auto) */
+    int32_t slab_ring;       /* TMEM slab form: load-ring stages per dot warp (1..16; 0 auto) */
+    int32_t reserved[3];
+} asy_tuning;
+
 typedef struct {
     int32_t mode;          /* ASY_MODE_* */
     int32_t schedule;      /* ASY_SCHED_* (async mode) */
@@ -133,8 +147,10 @@ typedef struct {
     double* x_out;         /* n entries or NULL: final x copied here */
     double* f_hist;        /* HOST array of `sweeps` entries or NULL: F(x) after every sweep */
     int32_t workers;       /* async: CTAs (0 = all resident) */
-    int32_t panel_rows;    /* dense async: rows per panel (0 = auto; multiple of 32, <= 256) */
-    int32_t stages;        /* dense async: smem pipeline stages (0 = auto) */
+    int32_t panel_rows;    /* panel kernel: rows per panel (0 = auto; multiple of 32, <= 256) */
+    int32_t stages;        /* panel kernel: smem stages (0 = auto, else 4 or 8).  A (panel_rows, stages)
+                              pair with no compiled kernel for the block width -> ASY_ERR_UNSUPPORTED */
+    const asy_tuning* tuning; /* NULL or overrides (see asy_tuning) */
 } asy_solve_params;
 
 typedef struct {

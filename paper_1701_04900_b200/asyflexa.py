@@ -51,12 +51,17 @@ class asy_problem(C.Structure):
                 ("lo_all", C.c_double), ("hi_all", C.c_double), ("block_size", C.c_int64)]
 
 
+class asy_tuning(C.Structure):
+    _fields_ = [("dense_kernel", C.c_int32), ("panel_park", C.c_int32), ("slab_hold", C.c_int32),
+                ("slab_chunk_rows", C.c_int32), ("slab_ring", C.c_int32), ("reserved", C.c_int32 * 3)]
+
+
 class asy_solve_params(C.Structure):
     _fields_ = [("mode", C.c_int32), ("schedule", C.c_int32), ("seed", C.c_uint64),
                 ("gamma", C.c_double), ("sweeps", C.c_int64), ("max_delay", C.c_int64),
                 ("reset", C.c_int32), ("x_mem", C.c_int32), ("x0", _vp), ("x_out", _vp),
                 ("f_hist", _vp), ("workers", C.c_int32), ("panel_rows", C.c_int32),
-                ("stages", C.c_int32)]
+                ("stages", C.c_int32), ("tuning", C.POINTER(asy_tuning))]
 
 
 class asy_solve_stats(C.Structure):
@@ -272,7 +277,9 @@ class Solver:
         self._registered = []
 
     def solve(self, *, mode=ASY_MODE_ASYNC, sweeps=1, gamma=None, schedule=ASY_SCHED_CYCLIC, seed=0,
-              max_delay=-1, reset=False, x0=None, f_hist=False, workers=0, panel_rows=0, stages=0):
+              max_delay=-1, reset=False, x0=None, f_hist=False, workers=0, panel_rows=0, stages=0,
+              tuning=None):
+        """tuning: None or a dict of asy_tuning fields (kernel choice / geometry overrides)."""
         sp = asy_solve_params()
         sp.mode, sp.schedule, sp.seed = mode, schedule, seed
         sp.gamma = self.P.gamma if gamma is None else gamma
@@ -286,6 +293,10 @@ class Solver:
         if f_hist:
             sp.f_hist = hist.ctypes.data
         sp.workers, sp.panel_rows, sp.stages = workers, panel_rows, stages
+        tu = None
+        if tuning:
+            tu = asy_tuning(**tuning)
+            sp.tuning = C.pointer(tu)
         st = asy_solve(self.h, sp)
         return (st, hist) if f_hist else st
 

@@ -30,6 +30,22 @@ using namespace asy;
 
 static std::string g_create_error;
 
+// Developer knobs (traces, segment profiles, geometry sweeps) exist only in a debug build
+// (-DASY_DEBUG_KNOBS: `python -m paper_1701_04900_b200.build --variant debug ASY_DEBUG_KNOBS`,
+// loaded with ASY_LIB_VARIANT=debug).  The product library reads no environment variable:
+// kernel choice and geometry overrides come through asy_solve_params.tuning.
+static const char* dbg_env(const char* name) {
+#ifdef ASY_DEBUG_KNOBS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
+static const asy_tuning kNoTuning{};
+static const asy_tuning& tuning_of(const asy_solve_params* sp) { return sp->tuning ? *sp->tuning : kNoTuning; }
+
 struct Dev {
     void* p = nullptr;
     size_t bytes = 0;
@@ -593,19 +609,22 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     // per-panel fixed costs dominate, not the load latency)
     int RPL = BT == 8 ? 8 : BT == 16 ? 8 : BT == 32 ? 4 : BT == 64 ? 2 : 1;
     int NS = kPairs;
-    if (getenv("ASY_DENSE_RPL")) RPL = atoi(getenv("ASY_DENSE_RPL"));
-    if (getenv("ASY_DENSE_NS")) NS = atoi(getenv("ASY_DENSE_NS"));
-    if (sp->panel_rows > 0) {
-        const int want = sp->panel_rows / 32;
-        if (dense_kernel_for(BT, want, NS, h->S.loss)) RPL = want;
-        else if (dense_kernel_for(BT, want, kPairs, h->S.loss)) { RPL = want; NS = kPairs; }
-    }
+    if (dbg_env("ASY_DENSE_RPL")) RPL = atoi(dbg_env("ASY_DENSE_RPL"));
+    if (dbg_env("ASY_DENSE_NS")) NS = atoi(dbg_env("ASY_DENSE_NS"));
+    // requested panel rows / stages: honoured when that (BT, RPL, NS) kernel is compiled, refused otherwise
+    if (sp->panel_rows > 0) RPL = sp->panel_rows / 32;
+    if (sp->stages > 0) NS = sp->stages;
+    else if (sp->panel_rows > 0 && !dense_kernel_for(BT, RPL, NS, h->S.loss) &&
+             dense_kernel_for(BT, RPL, 2 * kPairs, h->S.loss))
+        NS = 2 * kPairs;  // (only the rows were asked for: the stage count compiled for them)
     const int64_t R = 32 * RPL;
     const int64_t G = (h->m + R - 1) / R;
     DenseKernelFn fn = dense_kernel_for(BT, RPL, NS, h->S.loss);
-    if (!fn) return h->fail(ASY_ERR_UNSUPPORTED, "no dense kernel for BT=%d RPL=%d NS=%d", BT, RPL, NS);
+    if (!fn)
+        return h->fail(ASY_ERR_UNSUPPORTED, "panel kernel: no compiled geometry for %d-column blocks with %d panel rows "
+                       "and %d stages", BT, 32 * RPL, NS);
     int use_tmem = RPL * 2 * BT <= kSlotCols;
-    if (getenv("ASY_NO_TMEM")) use_tmem = 0;  // debug/test: force the re-read path
+    if (tuning_of(sp).panel_park == 2) use_tmem = 0;  // re-read panels from L2 instead of parking them
     constexpr int NAX = kPairs * kAxpyPerPair;
     const size_t smem = sizeof(double) * (NS * (R * BT + 2 * R) + NAX * BT) +
                         sizeof(StageMeta) * (NS + kQueue) + sizeof(Handoff) * NAX * kRing +
@@ -675,7 +694,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G; P.use_tmem = geo.use_tmem;
     // claims of 2 subtasks for narrow blocks (measured +4% on configs[1]), 4 otherwise (configs[2])
     P.claim = geo.Bpad <= 32 ? 2 : kClaim;
-    if (const char* e = getenv("ASY_CLAIM_N")) P.claim = std::max(1, std::min(kClaim, atoi(e)));
+    if (const char* e = dbg_env("ASY_CLAIM_N")) P.claim = std::max(1, std::min(kClaim, atoi(e)));
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
     P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;
@@ -687,11 +706,14 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.part = P_<double>(h->dpart); P.arrive = P_<unsigned>(h->arrive); P.consumed = P_<unsigned>(h->consumed);
     P.xver = P_<unsigned>(h->ver);
     P.slots = slots; P.Bmax = Bmax; P.Bpad = geo.Bpad;
+    TRY(dev_alloc(h, h->dobs, sizeof(unsigned)));
+    CK(cudaMemsetAsync(h->dobs.p, 0, sizeof(unsigned), h->stream));
+    P.dobs = P_<unsigned>(h->dobs);
     P.lg_slots = 0;
     while (((int64_t)1 << P.lg_slots) < slots) ++P.lg_slots;
 
     // debug trace (env ASY_TRACE=<subtasks>, ASY_TRACE_FILE=<path>): globaltimer stamps per subtask
-    const char* tr = getenv("ASY_TRACE");
+    const char* tr = dbg_env("ASY_TRACE");
     Dev trace;
     if (tr && atoll(tr) > 0) {
         P.trace_n = std::min<int64_t>(atoll(tr), P.T);
@@ -699,7 +721,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
         CK(cudaMemsetAsync(trace.p, 0, sizeof(unsigned long long) * 12 * P.trace_n, h->stream));
         P.trace = P_<unsigned long long>(trace);
     }
-    const char* pf = getenv("ASY_PROF");
+    const char* pf = dbg_env("ASY_PROF");
     Dev prof;
     if (pf) {
         TRY(dev_alloc(h, prof, sizeof(unsigned long long) * geo.grid * 16 * 8));
@@ -715,6 +737,11 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
+    {
+        unsigned dobs = 0;
+        CK(cudaMemcpy(&dobs, h->dobs.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        h->last_dobs = std::max(h->last_dobs, (int)dobs);
+    }
     if (sweeps & 1) std::swap(h->x, h->xalt);  // the updated iterate lives in the other half
     if (P.prof) {
         std::vector<unsigned long long> hb((size_t)geo.grid * 16 * 8);
@@ -729,7 +756,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     if (P.trace) {
         std::vector<unsigned long long> hb(12 * P.trace_n);
         CK(cudaMemcpy(hb.data(), trace.p, sizeof(unsigned long long) * hb.size(), cudaMemcpyDeviceToHost));
-        const char* fn = getenv("ASY_TRACE_FILE");
+        const char* fn = dbg_env("ASY_TRACE_FILE");
         FILE* f = fopen(fn ? fn : "asy_trace.bin", "wb");
         if (f) {
             fwrite(hb.data(), sizeof(unsigned long long), hb.size(), f);
@@ -784,7 +811,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // sub-sequence width: 32 columns (blocks of 65-128: four all-reduces per update overlap the
     // later columns' loads), the whole block for blocks of 33-64 (one all-reduce per update)
     int cs = bmax == 64 ? 64 : 32;
-    if (const char* e = getenv("ASY_SLABT_CS")) cs = (atoi(e) == 64 && bmax == 64) ? 64 : 32;
+    if (const char* e = dbg_env("ASY_SLABT_CS")) cs = (atoi(e) == 64 && bmax == 64) ? 64 : 32;
     const int CS = cs, nsplit = bmax / CS, SQ = 256 / CS;
     g->cs = cs;
     // slabs of whole 32-row groups: ngt groups over the CTAs, ngt / grid or one more each
@@ -806,15 +833,15 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // (a warp may start sub-sequence (k+1, h) once the all-reduce of (k, h - X) freed its slots);
     // the largest X <= 3 that leaves a load ring of >= 4 stages per warp
     int xmax = 3, xmin = 0;
-    if (const char* e = getenv("ASY_SLABT_EXTRA")) xmax = xmin = std::max(0, atoi(e));
+    if (const char* e = dbg_env("ASY_SLABT_EXTRA")) xmax = xmin = std::max(0, atoi(e));
     // the last, partial round of groups rotates over the warps (any warp may hold one of them)
     g->rotate = 1;
-    if (const char* e = getenv("ASY_SLABT_ROTATE")) g->rotate = atoi(e) != 0;
+    if (const char* e = dbg_env("ASY_SLABT_ROTATE")) g->rotate = atoi(e) != 0;
     // prefer a load ring of >= 8 stages per warp over spare park slots (configs[2]: 3.97 vs
     // 3.74 TB/s); only then settle for >= 4 stages
     int nsw = 0, nhold = 0;
-    const char* nsw_env = getenv("ASY_SLABT_NSW");  // (measurement / test override of the ring depth)
-    const int min_first = nsw_env ? std::max(1, atoi(nsw_env)) : 8, min_last = nsw_env ? min_first : 4;
+    const int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
+    const int min_first = ring > 0 ? ring : 8, min_last = ring > 0 ? min_first : 4;
     for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 4)
     for (int X = xmax; X >= xmin; --X) {
         nhold = 0;
@@ -827,7 +854,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
             nhold += hs;
         }
         nsw = kSlabTMaxStages / kSlabDot;
-        if (const char* e = getenv("ASY_SLABT_NSW")) nsw = std::max(1, std::min(nsw, atoi(e)));
+        if (ring > 0) nsw = std::max(1, std::min(nsw, ring));
         while (nsw > min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
         if (nsw >= min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
         nsw = 0;
@@ -888,14 +915,14 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     TRY(dev_alloc(h, h->dobs, sizeof(unsigned)));
     CK(cudaMemsetAsync(h->dobs.p, 0, sizeof(unsigned), h->stream));
     P.dobs = P_<unsigned>(h->dobs);
-    const char* pf = getenv("ASY_PROF");
+    const char* pf = dbg_env("ASY_PROF");
     Dev prof;
     if (pf) {
         TRY(dev_alloc(h, prof, sizeof(unsigned long long) * geo.grid * kSlabWarps * 8));
         CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * geo.grid * kSlabWarps * 8, h->stream));
         P.prof = P_<unsigned long long>(prof);
     }
-    if (getenv("ASY_SLAB_VERBOSE"))
+    if (dbg_env("ASY_SLAB_VERBOSE"))
         fprintf(stderr, "[slabt] grid %d Rs %lld bmax %d nsw %d nhold %d npark %d/%d/%d/%d smem %zu delay %lld det %d\n",
                 geo.grid, (long long)geo.Rs, geo.bmax, geo.nsw, geo.nhold, geo.npark[0], geo.npark[1], geo.npark[2],
                 geo.npark[3], geo.smem, (long long)delay, det);
@@ -930,9 +957,9 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
 static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay, float* ms) {
     {
         // the TMEM-parking form when its park ring fits (ASY_SLAB_TMEM=0: the smem / L2 form)
-        const char* te = getenv("ASY_SLAB_TMEM");
         SlabTGeom tg;
-        if ((!te || atoi(te) != 0) && slabt_geometry(h, sp, &tg)) return dense_slabt_launch(h, sp, tg, sweeps, delay, ms);
+        if (tuning_of(sp).dense_kernel != ASY_KERNEL_DENSE_SLAB && slabt_geometry(h, sp, &tg))
+            return dense_slabt_launch(h, sp, tg, sweeps, delay, ms);
     }
     const int64_t m = h->m, B = h->B;
     const int cpw = B <= 32 ? 8 : B <= 64 ? 16 : 32;
@@ -949,7 +976,7 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     // then fewest chunks, with stages of at most ~24 KB (ASY_SLAB_CHUNK_KB)
     int nch = 0, Rc = 0;
     {
-        const char* ckb = getenv("ASY_SLAB_CHUNK_KB");
+        const char* ckb = dbg_env("ASY_SLAB_CHUNK_KB");
         const int64_t chunk_bytes = 1024 * (ckb ? std::max(1, atoi(ckb)) : 24);
         const int64_t max_rows = std::max<int64_t>(2, std::min<int64_t>(256, (chunk_bytes / (8 * BMAX)) & ~1ll));
         int64_t best_waste = -1;
@@ -961,8 +988,8 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
             const int64_t waste = c * rc - Rs;
             if (best_waste < 0 || waste < best_waste) { best_waste = waste; nch = (int)c; Rc = (int)rc; }
         }
-        if (const char* e = getenv("ASY_SLAB_RC")) {  // debug override
-            Rc = std::max(2, std::min(256, atoi(e) & ~1));
+        if (const int rc = tuning_of(sp).slab_chunk_rows) {  // (test override)
+            Rc = std::max(2, std::min(256, rc & ~1));
             nch = (int)((Rs + Rc - 1) / Rc);
         }
     }
@@ -979,7 +1006,7 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     // dot stages come in per-dot-warp sub-rings (kSlabDot of them).  Hold the chunks until
     // the axpy when >= 2 sequences per dot warp fit, else re-load them from L2.
     int hold = total / kSlabDot >= 2 * nch;
-    if (const char* e = getenv("ASY_SLAB_HOLD")) hold = atoi(e) != 0 && total / kSlabDot >= nch + 1;
+    if (const int hv = tuning_of(sp).slab_hold) hold = hv == 1 && total / kSlabDot >= nch + 1;
     int nst, nsa;
     if (hold) {
         nst = std::min(total, kSlabMaxStages) / kSlabDot * kSlabDot;
@@ -995,7 +1022,7 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     // delay: the L2 must still hold a block between its dot pass and its re-load
     if (!hold) {
         const double blk_bytes = 8.0 * (double)m * (double)B;
-        const char* l2e = getenv("ASY_SLAB_L2MB");  // measurement override of the L2 budget
+        const char* l2e = dbg_env("ASY_SLAB_L2MB");  // measurement override of the L2 budget
         const double l2b = (l2e ? atof(l2e) : 40.0) * 1e6;
         const int64_t l2cap = std::max<int64_t>(1, (int64_t)(l2b / blk_bytes));
         delay = std::min(delay, l2cap);
@@ -1037,14 +1064,14 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
     P.K = sweeps * h->nblk; P.delay = delay; P.deterministic = det;
     P.gacc = P_<double>(h->gacc); P.part = det ? P_<double>(h->dpart) : nullptr; P.arrive = P_<unsigned>(h->arrive);
     P.slots = slots;
-    const char* pf = getenv("ASY_PROF");
+    const char* pf = dbg_env("ASY_PROF");
     Dev prof;
     if (pf) {
         TRY(dev_alloc(h, prof, sizeof(unsigned long long) * grid * kSlabWarps * 8));
         CK(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * grid * kSlabWarps * 8, h->stream));
         P.prof = P_<unsigned long long>(prof);
     }
-    if (getenv("ASY_SLAB_VERBOSE"))
+    if (dbg_env("ASY_SLAB_VERBOSE"))
         fprintf(stderr, "[slab] grid %d Rs %lld Rc %d nch %d hold %d nst %d nsa %d smem %zu delay %lld slots %lld det %d\n",
                 grid, (long long)Rs, Rc, nch, hold, nst, nsa, smem, (long long)delay, (long long)slots, det);
     slab_init<<<grid_for(2 * slots * kGaccRep * B, 256, 4 * h->sms), 256, 0, h->stream>>>(P);
@@ -1074,11 +1101,10 @@ static int dense_slab_launch(asy_handle* h, const asy_solve_params* sp, int64_t 
 // update is large (>= 64 KB: tall and wide blocks, e.g. configs[2] and [3]); the TMEM panel
 // kernel otherwise (a block update touches only G of the SMs, no global all-reduce per
 // update).  ASY_DENSE_KERNEL=panel|slab overrides (tests, measurements).
-static bool use_slab_kernel(const asy_handle* h) {
-    if (const char* kv = getenv("ASY_DENSE_KERNEL")) {
-        if (!strcmp(kv, "panel")) return false;
-        if (!strcmp(kv, "slab")) return true;
-    }
+static bool use_slab_kernel(const asy_handle* h, const asy_solve_params* sp) {
+    const int want = tuning_of(sp).dense_kernel;
+    if (want == ASY_KERNEL_DENSE_PANEL) return false;
+    if (want == ASY_KERNEL_DENSE_SLAB || want == ASY_KERNEL_DENSE_SLAB_TMEM) return true;
     // (measured: configs[2], 69 KB per SM per update: slab 3.74 TB/s vs panel 3.22; configs[1],
     // 17 KB: panel 4.4 vs slab 1.8)
     const double per_sm = 8.0 * (double)h->B * (double)h->m / (double)std::max(1, h->sms);
@@ -1152,6 +1178,14 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     if (sp->panel_rows < 0 || (sp->panel_rows % 32) || sp->panel_rows > 256)
         return h->fail(ASY_ERR_INVALID, "panel_rows must be a multiple of 32 in [0, 256]");
     if (sp->stages < 0 || sp->stages > 16) return h->fail(ASY_ERR_INVALID, "stages must be in [0,16]");
+    if (sp->tuning) {
+        const asy_tuning& t = *sp->tuning;
+        if ((t.dense_kernel != 0 && t.dense_kernel != ASY_KERNEL_DENSE_PANEL && t.dense_kernel != ASY_KERNEL_DENSE_SLAB &&
+             t.dense_kernel != ASY_KERNEL_DENSE_SLAB_TMEM) ||
+            (t.panel_park != 0 && t.panel_park != 2) || t.slab_hold < 0 || t.slab_hold > 2 || t.slab_chunk_rows < 0 ||
+            t.slab_chunk_rows > 256 || t.slab_ring < 0 || t.slab_ring > 16)
+            return h->fail(ASY_ERR_INVALID, "bad asy_tuning field");
+    }
     CK(cudaSetDevice(h->device));
     asy_solve_stats stats{};
     h->last_dobs = -1;
@@ -1178,7 +1212,7 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
         } else {
             float ms = 0;
             if (h->kind == ASY_DENSE_COLMAJOR) {
-                bool slab = use_slab_kernel(h), too_tall = false;
+                bool slab = use_slab_kernel(h, sp), too_tall = false;
                 if (!slab) {
                     const int rc = dense_async_launch(h, sp, chunk, delay, &ms, &too_tall);
                     if (rc != ASY_OK && !too_tall) return rc;

@@ -46,9 +46,13 @@
 // strictly older sequences -> deadlock free with co-resident CTAs):
 //   * D4 freshness [PAPER.md:233]: block b is not read before its previous
 //     update is complete -- applied to r and written to x (xver[b] = u*G);
-//   * bounded delay D1 [PAPER.md:224]: sequence k does not read before
-//     sequence k - delay - 1 is complete;
-//   * slot reuse: sequence k - S (previous user of the slot) is complete.
+//   * bounded delay D1 [PAPER.md:224]: sequence k does not read before EVERY
+//     sequence up to k - delay - 1 is complete.  Each scheduler keeps an in-order
+//     watermark wm (all sequences < wm complete) and advances it over the completion
+//     counters in sequence order, so sequences finishing out of order across CTAs never
+//     let a read run more than delay updates ahead of the oldest missing one;
+//   * slot reuse: sequence k - S (previous user of the slot) is complete -- implied by
+//     the watermark (S > delay + 1).
 // delay == 0 makes the kernel the sequential (d^k = 0) scheme and, with the
 // fixed-order partial reduction (deterministic = 1), bit-reproducible.
 #pragma once
@@ -78,7 +82,11 @@ constexpr int kRoll = ASY_ROLL;
 #ifndef ASY_CLAIM
 #define ASY_CLAIM 4  // most subtasks claimed per atomic (runtime: DenseAsyncParams::claim)
 #endif
+#ifndef ASY_PROXY_FENCE
+#define ASY_PROXY_FENCE 1
+#endif
 constexpr int kQueue = ASY_QUEUE;    // scheduler -> producer queue depth
+constexpr int kWm = 8;               // completion counters loaded per batch past the D1 watermark
 constexpr int kRing = 32;            // hand-off notes per axpy warp
 constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
 constexpr int kClaim = ASY_CLAIM;    // subtasks claimed per atomic
@@ -131,6 +139,8 @@ struct DenseAsyncParams {
     int lg_slots;        // log2(slots)
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
+    unsigned* dobs;             // observed delay: max over admitted subtasks of k - (first sequence
+                                // not known complete), an upper bound on d^k of Assumption D1
     unsigned long long* prof;   // optional [grid][warps][8] clock64 segment sums (debug; null = off)
     unsigned long long* trace;  // optional [trace_n][8] globaltimer stamps (debug; null = off)
     int64_t trace_n;
@@ -412,6 +422,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const long long nr = (P.m - r0) < R ? (P.m - r0) : R;
                 const uint32_t rbytes = (uint32_t)(((nr + 1) & ~1ll) * 8);
                 double* dst = stages + st * STAGE;
+#if ASY_PROXY_FENCE
+                // the residual rows were updated by other SMs' red.adds (generic proxy) and are read
+                // by the bulk copy (async proxy): order the scheduler's acquire before the copy
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
                 mbar_arrive_expect_tx(&full[st], box_bytes + 2 * rbytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
                 bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
@@ -438,12 +453,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const int half = perm_half_bits(N);
             PermKeys pk{};
             long long ck = -1, cb = 0, cu = 0, cE = -1;  // cached sequence / block / epochs
+            long long wm = 0;    // in-order watermark: every sequence < wm is complete
+            long long dmax = 0;  // observed delay (max k - wm at admission)
             const int nclaim = P.claim;
             long long tb = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
             while (tb < P.T) {
                 const long long tn = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
                 StageMeta e[kClaim];
-                unsigned xv[kClaim], cs[kClaim], cw[kClaim];
+                unsigned xv[kClaim];
                 long long k = tb / G, p = tb - k * G;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
@@ -473,35 +490,54 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     ASY_TRACE(P, t, 0);
                     if (++p == G) { p = 0; ++k; }
                 }
-                // guards: all loads in flight at once
+                // guards: all loads in flight at once -- block freshness (D4) per subtask and the
+                // completion counters of the next kWm sequences past the watermark (D1, slot reuse)
+                long long kdmax = -1;
 #pragma unroll
-                for (int i = 0; i < kClaim; ++i) {
-                    const long long kk = e[i].k, kd = kk - P.delay - 1;
-                    if (e[i].t < 0) { xv[i] = cs[i] = cw[i] = 0u; continue; }
-                    xv[i] = ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]);
-                    cs[i] = ld_relaxed_u32(&P.consumed[(kk & (P.slots - 1)) * kCtrPad]);
-                    cw[i] = kd >= 0 ? ld_relaxed_u32(&P.consumed[(kd & (P.slots - 1)) * kCtrPad]) : 0u;
+                for (int i = 0; i < kClaim; ++i)
+                    if (e[i].t >= 0) kdmax = e[i].k - P.delay - 1;
+                unsigned cwl[kWm];
+#pragma unroll
+                for (int u = 0; u < kWm; ++u) {
+                    const long long sq = wm + u;
+                    cwl[u] = sq <= kdmax ? ld_relaxed_u32(&P.consumed[(sq & (P.slots - 1)) * kCtrPad]) : 0u;
+                }
+#pragma unroll
+                for (int i = 0; i < kClaim; ++i)
+                    xv[i] = e[i].t >= 0 ? ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]) : 0u;
+                // advance the watermark over the sequences already complete, in order
+                {
+                    bool run = true;
+#pragma unroll
+                    for (int u = 0; u < kWm; ++u) {
+                        const long long sq = wm;
+                        run = run && sq <= kdmax && cwl[u] >= (unsigned)((sq >> lgS) + 1) * (unsigned)G;
+                        if (run) ++wm;
+                    }
                 }
                 // admit in claim order: a subtask never waits while an older one of this batch is
-                // held back.  Guards are observed with relaxed loads: the TMA reads residual rows
-                // and A from L2 (never through L1), and the counters were released (after a fence)
-                // by the SMs that completed the updates, so nothing stale can be read; a fence
-                // follows only a guard that had to wait.
+                // held back.  Polls are relaxed (ld.acquire would invalidate the SM's L1 on every
+                // poll); one fence per batch then orders the admitted reads after the observed
+                // completions (acquire), before the producer's bulk copies read r.
+                bool waited = false;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     if (e[i].t < 0) continue;
                     const long long kk = e[i].k, kd = kk - P.delay - 1;
-                    const unsigned Gu = (unsigned)G;
-                    const unsigned need_x = (unsigned)e[i].u * Gu;                         // previous update of b
-                    const unsigned need_s = (unsigned)(kk >> lgS) * Gu;                    // seq k - S complete
-                    const unsigned need_w = kd >= 0 ? (unsigned)((kd >> lgS) + 1) * Gu : 0u;  // seq kd complete
-                    if (xv[i] < need_x || cs[i] < need_s || cw[i] < need_w) {
-                        // relaxed polls (ld.acquire would invalidate the SM's L1 on every poll)
-                        spin_until_ge_relaxed(&P.xver[e[i].b * kCtrPad], need_x);
-                        spin_until_ge_relaxed(&P.consumed[(kk & (P.slots - 1)) * kCtrPad], need_s);
-                        if (kd >= 0) spin_until_ge_relaxed(&P.consumed[(kd & (P.slots - 1)) * kCtrPad], need_w);
-                        fence_acqrel_gpu();
+                    while (wm <= kd) {  // D1: every sequence up to kd complete
+                        spin_until_ge_relaxed(&P.consumed[(wm & (P.slots - 1)) * kCtrPad],
+                                              (unsigned)((wm >> lgS) + 1) * (unsigned)G);
+                        ++wm;
+                        waited = true;
                     }
+                    const unsigned need_x = (unsigned)e[i].u * (unsigned)G;  // previous update of b (D4)
+                    if (xv[i] < need_x) {
+                        spin_until_ge_relaxed(&P.xver[e[i].b * kCtrPad], need_x);
+                        waited = true;
+                    }
+                    if (kk - wm > dmax) dmax = kk - wm;
+                    if (i == 0 || waited) fence_acqrel_gpu();
+                    waited = false;
                     push(e[i]);
                 }
                 tb = tn;
@@ -509,6 +545,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             StageMeta end;
             end.t = -1; end.k = end.b = end.p = end.u = 0;
             push(end);
+            if (P.dobs && dmax > 0) atomicMax(P.dobs, (unsigned)dmax);
         }
         __syncwarp();
     } else if (warp >= kPairs && warp < 2 * kPairs) {

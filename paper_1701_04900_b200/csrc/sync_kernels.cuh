@@ -194,9 +194,9 @@ __device__ __forceinline__ void block_reduce_store(double (&v)[kRedVals], const 
     }
 }
 
-// partial[cta][0..5] = { sum phi(r), sum x^2, sum h(x), #out-of-box, sum mf^2, max|mf| } and
-// (stationarity only) slot 5 = max(max|mf|, ...) ; merit reduced separately via slot 3 reuse? no:
-// slots: 0 sum loss, 1 sum x^2, 2 sum h(x), 3 box violations, 4 sum mf^2, 5 max |mf|
+// partial[cta][0..5] = { sum phi(r), sum x^2, sum h(x), #out-of-box coordinates, sum mf^2,
+// max |mf| } (mf = M_F(x) of Eq. 5, only when the stationarity call passes it; the Sec. 4.3
+// merit is reduced by max_partial_kernel from its own per-coordinate array)
 __global__ void objective_partial_kernel(Scalars S, const double* __restrict__ r,
                                          const double* __restrict__ aux, int64_t m,
                                          const double* __restrict__ x, int64_t n,

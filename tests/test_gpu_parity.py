@@ -240,36 +240,39 @@ def test_async_long_launch_slot_reuse_ragged(A):
         S.close()
 
 
+PANEL, SLAB, SLABT = 1, 2, 4  # ASY_KERNEL_DENSE_PANEL / _SLAB (smem/L2 form) / _SLAB_TMEM (asy_tuning.dense_kernel)
 DENSE_VARIANTS = {
     # smem / L2 form of the slab kernel
-    "slab_hold": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_HOLD": "1"},   # axpy reads the dot pass's chunk
-    "slab_reload": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_HOLD": "0"},  # axpy re-loads the chunk (L2)
-    "slab_chunks": {"ASY_DENSE_KERNEL": "slab", "ASY_SLAB_TMEM": "0", "ASY_SLAB_RC": "8"},    # many chunks per sequence
+    "slab_hold": {"dense_kernel": SLAB, "slab_hold": 1},          # axpy reads the dot pass's chunk
+    "slab_reload": {"dense_kernel": SLAB, "slab_hold": 2},        # axpy re-loads the chunk (L2)
+    "slab_chunks": {"dense_kernel": SLAB, "slab_chunk_rows": 8},  # many chunks per sequence
     # TMEM-parking form of the slab kernel (dense_slabt.cuh)
-    "slabt": {"ASY_DENSE_KERNEL": "slab"},
-    "slabt_nsw2": {"ASY_DENSE_KERNEL": "slab", "ASY_SLABT_NSW": "2"},
-    "panel": {"ASY_DENSE_KERNEL": "panel"},           # TMEM panel kernel
-    "panel_reread": {"ASY_DENSE_KERNEL": "panel", "ASY_NO_TMEM": "1"},
+    "slabt": {"dense_kernel": SLABT},
+    "slabt_nsw2": {"dense_kernel": SLABT, "slab_ring": 2},
+    "panel": {"dense_kernel": PANEL},                             # TMEM panel kernel
+    "panel_reread": {"dense_kernel": PANEL, "panel_park": 2},
 }
 
 
 @pytest.mark.parametrize("variant", sorted(DENSE_VARIANTS))
 @pytest.mark.parametrize("case", ["dense_ragged", "large_block", "nonconvex"])
-def test_dense_kernel_variants(A, case, variant, monkeypatch):
+def test_dense_kernel_variants(A, case, variant):
     """Every geometry / code path of the dense asynchronous kernels: sequential parity
     (per iteration) and asynchronous convergence to the oracle's solution."""
-    for k, v in DENSE_VARIANTS[variant].items():
-        monkeypatch.setenv(k, v)
+    T = DENSE_VARIANTS[variant]
     P = make_case(case)
     S = A.Solver(P)
     try:
-        S.solve(sweeps=4, max_delay=0, reset=True)
+        st = S.solve(sweeps=4, max_delay=0, reset=True, tuning=T)
+        want = {PANEL: [A.ASY_KERNEL_DENSE_PANEL], SLAB: [A.ASY_KERNEL_DENSE_SLAB],
+                SLABT: [A.ASY_KERNEL_DENSE_SLAB_TMEM, A.ASY_KERNEL_DENSE_SLAB]}[T["dense_kernel"]]
+        assert st.kernel in want
         x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 4))
         assert _rel_x(S.x(), x_or) <= REL
         F_star = fstar(P)
         S.solve(sweeps=0, reset=True)
         for _ in range(60):
-            S.solve(sweeps=100, schedule=A.ASY_SCHED_RANDOM, seed=5)
+            S.solve(sweeps=100, schedule=A.ASY_SCHED_RANDOM, seed=5, tuning=T)
             out = S.stationarity()
             meas = out.merit_inf if P.c > 0 else out.mf_norm2
             if _rel_f(out.objective, F_star) <= 1e-6 and meas <= 1e-5:
@@ -281,18 +284,16 @@ def test_dense_kernel_variants(A, case, variant, monkeypatch):
 
 @pytest.mark.parametrize("kernel", ["slab", "slab_smem", "panel"])
 @pytest.mark.parametrize("workers", [1, 3, 37])
-def test_dense_few_workers(A, workers, kernel, monkeypatch):
+def test_dense_few_workers(A, workers, kernel):
     """Fewer CTAs than SMs (taller row slabs / fewer panel workers), same results."""
-    monkeypatch.setenv("ASY_DENSE_KERNEL", kernel.split("_")[0])
-    if kernel == "slab_smem":
-        monkeypatch.setenv("ASY_SLAB_TMEM", "0")
+    T = {"dense_kernel": {"slab": SLABT, "slab_smem": SLAB, "panel": PANEL}[kernel]}
     P = make_case("dense_ragged")
     S = A.Solver(P)
     try:
-        S.solve(sweeps=3, max_delay=0, reset=True, workers=workers)
+        S.solve(sweeps=3, max_delay=0, reset=True, workers=workers, tuning=T)
         x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 3))
         assert _rel_x(S.x(), x_or) <= REL
-        S.solve(sweeps=200, reset=True, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=1)
+        S.solve(sweeps=200, reset=True, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=1, tuning=T)
         F_star = fstar(P)
         out = S.stationarity()
         assert _rel_f(out.objective, F_star) <= 1e-6 and out.mf_norm2 <= 1e-5
@@ -304,24 +305,24 @@ def test_dense_few_workers(A, workers, kernel, monkeypatch):
                                           ("dense_ragged", 1), ("dense_ragged", 2), ("nonconvex", 1),
                                           ("dense_logistic", 1), ("box64", 1), ("box64", 2), ("block100", 1),
                                           ("block100", 3), ("block100", 0), ("dc_exp", 1), ("dc_log", 2)])
-def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
+def test_slab_tmem_tall_slabs(A, case, workers):
     """TMEM-parking slab kernel with tall slabs: several 32-row groups per dot warp, a ragged
     last group (1-D bulk copies), hold slots in shared memory when a warp owns more groups than
     its TMEM lane quarter holds (tall_block, 1 worker: 9 groups of 128 columns), park rings
     that wrap many times.  Sequential parity per sweep, then asynchronous convergence."""
-    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    T = {"dense_kernel": SLABT}
     P = make_case(case)
     S = A.Solver(P)
     try:
         for sweeps in (1, 3):
-            st = S.solve(sweeps=sweeps, max_delay=0, reset=True, workers=workers)
+            st = S.solve(sweeps=sweeps, max_delay=0, reset=True, workers=workers, tuning=T)
             assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
             x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, sweeps))
             assert _rel_x(S.x(), x_or) <= REL
         F_star = fstar(P)
         S.solve(sweeps=0, reset=True)
         for _ in range(60):
-            st = S.solve(sweeps=100, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=3)
+            st = S.solve(sweeps=100, workers=workers, schedule=A.ASY_SCHED_RANDOM, seed=3, tuning=T)
             assert 0 <= st.delay_observed <= st.delay  # Assumption D1 holds as enforced
             out = S.stationarity()
             meas = out.merit_inf if P.c > 0 else out.mf_norm2
@@ -333,14 +334,14 @@ def test_slab_tmem_tall_slabs(A, case, workers, monkeypatch):
 
 
 @pytest.mark.parametrize("case,workers", [("tall_block", 1), ("large_block", 3), ("box64", 2), ("dense_ragged", 1)])
-def test_slab_tmem_sequential_random_schedule(A, case, workers, monkeypatch):
+def test_slab_tmem_sequential_random_schedule(A, case, workers):
     """TMEM slab kernel, sequential mode, seeded Philox/Feistel schedule: D4 through the inverse
     permutation (schedule_prev) and the rotating partial round of groups, per-sweep parity."""
-    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    T = {"dense_kernel": SLABT}
     P = make_case(case)
     S = A.Solver(P)
     try:
-        st = S.solve(sweeps=3, max_delay=0, schedule=A.ASY_SCHED_RANDOM, seed=41, reset=True, workers=workers)
+        st = S.solve(sweeps=3, max_delay=0, schedule=A.ASY_SCHED_RANDOM, seed=41, reset=True, workers=workers, tuning=T)
         assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
         assert st.delay_observed == 0  # sequential: every read sees all earlier updates
         x_or, _ = O.run_sequential(P, P.gamma, O.random_schedule(41, P.nblocks, 3))
@@ -350,18 +351,18 @@ def test_slab_tmem_sequential_random_schedule(A, case, workers, monkeypatch):
         S.close()
 
 
-def test_slab_fallback_when_too_tall(A, monkeypatch):
+def test_slab_fallback_when_too_tall(A):
     """A slab of 19 row groups (> 4 per dot warp) does not fit the TMEM park ring: the
     dispatcher falls back to the smem/L2 slab form, with the same results."""
-    monkeypatch.setenv("ASY_DENSE_KERNEL", "slab")
+    T = {"dense_kernel": SLABT}
     P = make_case("tall600")
     S = A.Solver(P)
     try:
-        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=1)
+        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=1, tuning=T)
         assert st.kernel == A.ASY_KERNEL_DENSE_SLAB and st.delay_observed == -1
         x_or, _ = O.run_sequential(P, P.gamma, O.cyclic_schedule(P.nblocks, 3))
         assert _rel_x(S.x(), x_or) <= REL
-        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=8)  # 3 groups per slab: TMEM form
+        st = S.solve(sweeps=3, max_delay=0, reset=True, workers=8, tuning=T)  # 3 groups per slab: TMEM form
         assert st.kernel == A.ASY_KERNEL_DENSE_SLAB_TMEM
         assert _rel_x(S.x(), x_or) <= REL
     finally:
@@ -431,6 +432,18 @@ def test_invalid_arguments(A):
         S.solve(gamma=1.5)
     with pytest.raises(A.AsyError):
         S.solve(panel_rows=48)
+    # a (panel_rows, stages) pair with no compiled kernel is refused, not silently replaced
+    with pytest.raises(A.AsyError) as e:
+        S.solve(panel_rows=32, tuning={"dense_kernel": PANEL})
+    assert e.value.code == A.ASY_ERR_UNSUPPORTED
+    with pytest.raises(A.AsyError) as e:
+        S.solve(stages=6, tuning={"dense_kernel": PANEL})
+    assert e.value.code == A.ASY_ERR_UNSUPPORTED
+    with pytest.raises(A.AsyError) as e:
+        S.solve(tuning={"dense_kernel": 3})
+    assert e.value.code == A.ASY_ERR_INVALID
+    st = S.solve(sweeps=1, panel_rows=96, tuning={"dense_kernel": PANEL})  # (32, 3, 8) is compiled
+    assert st.kernel == A.ASY_KERNEL_DENSE_PANEL
     S.close()
     P.block = 0
     with pytest.raises(A.AsyError):
