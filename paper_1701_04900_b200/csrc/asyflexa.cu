@@ -1126,9 +1126,18 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     // batch size: 32 / LPC updates per warp, at most delay + 1 (a batch never waits for itself)
     const int BS = (int)std::min<int64_t>(32 / LPC, delay + 1);
     const int64_t NB = (h->n + BS - 1) / BS;
-    const int64_t warps = (int64_t)grid * (kSparseThreads / 32);
-    const int64_t slots = next_pow2(std::max<int64_t>(1024, delay / BS + 4 * warps + 64));
-    TRY(dev_alloc(h, h->done, sizeof(long long) * slots));
+    // D1 window counters (sparse_async.cuh): W <= ceil((delay + 2) / BS) - 1 batches per window
+    // (the windows a batch waits for end before it); S > (delay + 2) / W + 2 slots (a window is
+    // reused only after it completed: delay + 2 sequences span at most delay + 2 batches)
+    // (and W <= a sixteenth of the batches the delay spans: the window granularity then costs
+    // little of the allowed delay)
+    const int64_t wmax = std::max<int64_t>(1, std::min<int64_t>((delay + 2 + BS - 1) / BS - 1, (delay / BS) / 16));
+    int lgW = 0;
+    while (lgW < 6 && ((int64_t)2 << lgW) <= wmax) ++lgW;
+    const int64_t slots = next_pow2(std::max<int64_t>(256, ((delay + 2) >> lgW) + 8));
+    int lgS = 0;
+    while (((int64_t)1 << lgS) < slots) ++lgS;
+    TRY(dev_alloc(h, h->done, sizeof(unsigned) * slots));
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->n));
     TRY(dev_alloc(h, h->rs, sizeof(double) * 2 * h->m));  // [r_i, aux_i] pairs for the launch
     TRY(dev_alloc(h, h->dobs, sizeof(unsigned)));
@@ -1138,8 +1147,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     P.tau = P_<double>(h->tau); P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed;
     P.epoch0 = h->epochs; P.T = sweeps * NB; P.NB = NB; P.BS = BS; P.delay = delay;
     P.counter = P_<unsigned long long>(h->counter);
-    P.gwm = P_<unsigned long long>(h->counter) + 4;  // (another 32-byte sector of the counter line)
-    P.ver = P_<unsigned>(h->ver); P.done = P_<long long>(h->done); P.slots = slots;
+    P.ver = P_<unsigned>(h->ver); P.wcnt = P_<unsigned>(h->done); P.lgW = lgW; P.lgS = lgS;
     P.dobs = P_<unsigned>(h->dobs);
     h->last_kernel = ASY_KERNEL_SPARSE;
     h->last_delay = (int)delay;

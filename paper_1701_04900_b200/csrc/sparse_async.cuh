@@ -15,18 +15,21 @@
 //
 // Guards (checked for the whole batch before it reads; all point to strictly older
 // batches, so co-resident warps cannot deadlock):
-//   * bounded delay D1 [PAPER.md:224] with an in-order watermark: `gwm` is the number of
-//     leading batches that are complete; batch t reads only when every sequence up to
-//     k_max(t) - delta - 1 is complete, i.e. gwm > batch(k_max - delta - 1).  BS <= delta + 1
-//     keeps that batch strictly older than t.  The warp that completes batch t marks
-//     done[t mod S] = t and, if gwm == t, advances gwm over t and every later batch already
-//     marked (a fence.sc between the mark and the watermark read on both sides, so two
-//     warps finishing adjacent batches cannot both miss each other);
+//   * bounded delay D1 [PAPER.md:224] through window counters: batches are grouped in windows
+//     of W consecutive batches; the warp that completes batch t adds 1 to wcnt[(t / W) mod S]
+//     (monotone: window w is complete when its slot holds (w / S + 1) W).  Batch t reads only
+//     when every window that holds a batch up to batch(k_max(t) - delta - 1) is complete (all
+//     such batches applied, so D1 holds exactly).  No warp ever walks a global watermark: each
+//     warp keeps its own count of leading complete windows and advances it 32 windows per
+//     L2 round trip (one counter per lane, ballot).  The host picks W <= ceil((delta + 2) / BS) - 1,
+//     so those windows end strictly before batch t, and S > (delta + 2) / W + 2, so a slot
+//     is reused only after its previous window is complete;
 //   * own-block freshness D4 [PAPER.md:233]: ver[j] = number of applied updates of block j;
 //     the update of epoch e waits for ver[j] >= e.
-// delta == 0 gives BS = 1 and the sequential (d^k = 0) scheme, bit-reproducible.
-// Observed delay: the largest k - k_first(gwm) over the batch's sequences at read time (an
-// upper bound on d^k of Assumption D1: every update before batch gwm was applied).
+// delta == 0 gives BS = W = 1 and the sequential (d^k = 0) scheme, bit-reproducible.
+// Observed delay: sampled on every 32nd batch of a warp, after a refresh of its window count wm:
+// the largest k - k_first(W * wm) over the batch's sequences at read time (an upper bound on d^k
+// of Assumption D1 at that read: every update before batch W * wm was applied).
 #pragma once
 #include "common.cuh"
 
@@ -50,10 +53,10 @@ struct SparseAsyncParams {
     int BS;           // block updates per batch (<= 32 / LPC, <= delay + 1)
     int64_t delay;
     unsigned long long* counter;  // batch claims
-    unsigned long long* gwm;      // in-order completion watermark (batches)
     unsigned* ver;                // [n]
-    long long* done;              // [S] done[t mod S] = t once batch t is complete
-    int64_t slots;                // S, power of two
+    unsigned* wcnt;               // [S] completed batches of window w at slot w mod S (monotone)
+    int lgW;                      // W = 2^lgW batches per window
+    int lgS;                      // S = 2^lgS window slots
     unsigned* dobs;               // observed delay (max)
 };
 
@@ -104,10 +107,9 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     if (tid == 0) {
         *P.counter = 0ull;
-        *P.gwm = 0ull;
         *P.dobs = 0u;
     }
-    for (int64_t s = tid; s < P.slots; s += nth) P.done[s] = -1;
+    for (int64_t s = tid; s < ((int64_t)1 << P.lgS); s += nth) P.wcnt[s] = 0u;
     for (int64_t j = tid; j < P.n; j += nth) P.ver[j] = 0u;
 }
 
@@ -129,7 +131,10 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
     const int64_t N = P.n, NB = P.NB;
     const int BS = P.BS;
     const int half = perm_half_bits(N);
-    const int64_t S = P.slots;
+    const int lgW = P.lgW, lgS = P.lgS;
+    const long long Smask = (1ll << lgS) - 1;
+    long long wmw = 0;  // this warp's count of leading complete windows (warp-uniform)
+    unsigned iter = 0;
     PermKeys pk{};
     int64_t pkE = -1;
     unsigned dmax = 0;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
     auto batch_of = [&](long long k) { const int64_t e = k / N; return e * NB + (k - e * N) / BS; };
 
     // completion of batch t (after its scatter): fence (the batch's r red.adds and x stores
-    // first), per-block versions, the batch mark, and the in-order watermark advance
+    // first), per-block versions, and one count on the batch's window
     long long pend = -1;
     int64_t pend_j = 0;
     bool pend_live = false;
@@ -188,18 +193,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
         if (pend < 0) return;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");  // every lane: its own atomics / x store
         if (pend_live && el == 0) red_relaxed_u32_g(&P.ver[pend_j], 1u);
-        __syncwarp();
-        if (lane == 0) {
-            st_relaxed_s64_g(&P.done[pend & (S - 1)], pend);
-            asm volatile("fence.sc.gpu;" ::: "memory");
-            unsigned long long t = (unsigned long long)pend;
-            for (;;) {
-                if (atomicCAS(P.gwm, t, t + 1) != t) break;  // an older batch is still running
-                ++t;
-                asm volatile("fence.sc.gpu;" ::: "memory");
-                if (ld_relaxed_s64_g(&P.done[t & (S - 1)]) != (long long)t) break;
-            }
-        }
+        if (lane == 0) red_relaxed_u32_g(&P.wcnt[(pend >> lgW) & Smask], 1u);
         pend = -1;
     };
 
@@ -209,29 +203,34 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
         const Head cur = nx;
         // previous batch's completion (its fence also waits for this head's loads)
         complete();
-        // D1: every sequence up to k_max - delta - 1 complete (in-order watermark)
+        // D1: every window holding a batch up to batch(k_max - delta - 1) complete
         {
             const int64_t i0 = (cur.t - cur.e * NB) * (int64_t)BS;
             const int64_t nlive = (N - i0) < BS ? (N - i0) : BS;
             const long long kmax = cur.e * N + i0 + nlive - 1;
             const long long kd = kmax - P.delay - 1;
-            unsigned long long w = 0;
-            if (lane == 0) {
-                w = ld_relaxed_u64_g(P.gwm);
-                if (kd >= 0) {
-                    const unsigned long long need = (unsigned long long)batch_of(kd) + 1ull;
-                    unsigned ns = 32;
-                    while (w < need) {
-                        __nanosleep(ns);
-                        if (ns < 256) ns <<= 1;
-                        w = ld_relaxed_u64_g(P.gwm);
-                    }
+            // every 32nd batch of a warp refreshes its window count even when the guard holds (the
+            // observed delay below is then the real lag of the residual, not of a stale count)
+            const long long nw = kd >= 0 ? (batch_of(kd) + (1ll << lgW)) >> lgW : 0;  // windows needed
+            const bool sample = (++iter & 31) == 0;
+            if (wmw < nw || sample) {
+                unsigned ns = 32;
+                for (;;) {
+                    // lane l: is window wmw + l complete?
+                    const long long w = wmw + lane;
+                    const unsigned c = ld_relaxed_u32_g(&P.wcnt[w & Smask]);
+                    const bool ok = c >= (unsigned)(((w >> lgS) + 1) << lgW);
+                    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                    wmw += bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
+                    if (bal == 0xffffffffu) continue;  // maybe more complete windows
+                    if (wmw >= nw) break;
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
                 }
             }
-            w = __shfl_sync(0xffffffffu, w, 0);
-            // observed delay: sequences before batch w are all applied
-            if (cur.live && el == 0) {
-                const long long miss = cur.k - kfirst((long long)w);
+            // observed delay: sequences before batch W * wmw are all applied
+            if (sample && cur.live && el == 0) {
+                const long long miss = cur.k - kfirst(wmw << lgW);
                 if (miss > (long long)dmax) dmax = (unsigned)miss;
             }
         }
