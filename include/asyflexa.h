@@ -130,7 +130,10 @@ typedef struct {
     int32_t slab_hold;       /* smem/L2 slab form: 0 auto, 1 hold the chunks in smem, 2 re-load them from L2 */
     int32_t slab_chunk_rows; /* smem/L2 slab form: rows per chunk (even, <= 256; 0 auto) */
     int32_t slab_ring;       /* TMEM slab form: load-ring stages per dot warp (1..16; 0 auto) */
-    int32_t reserved[3];
+    int32_t measure_delay;   /* 1: the panel and CSC kernels sample the observed delay
+                                (asy_solve_stats.delay_observed) -- a measurement mode: its polls of
+                                counters under heavy atomic traffic slow the kernels (~9%) */
+    int32_t reserved[2];
 } asy_tuning;
 
 typedef struct {
@@ -163,10 +166,11 @@ typedef struct {
     int32_t kernel;          /* update kernel of the last launch: ASY_KERNEL_* */
     int32_t delay;           /* async: bounded delay actually enforced (<= max_delay; capped by the
                                 kernel's buffering), -1 for Jacobi */
-    int32_t delay_observed;  /* async, TMEM row-slab kernel: the largest number of earlier block
-                                updates missing from the residual rows a gradient was read from
-                                (observed delay, Assumption D1 [PAPER.md:224]; <= delay); -1 when the
-                                kernel that ran does not measure it */
+    int32_t delay_observed;  /* async: the largest number of earlier block updates missing from the
+                                residual a gradient was read from (observed delay d^k, Assumption D1
+                                [PAPER.md:224]; <= delay).  Always measured by the TMEM row-slab kernel;
+                                by the panel and CSC kernels only with asy_tuning.measure_delay = 1
+                                (sampled, an upper bound); -1 when not measured */
 } asy_solve_stats;
 
 typedef struct {

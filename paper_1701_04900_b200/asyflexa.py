@@ -53,7 +53,8 @@ class asy_problem(C.Structure):
 
 class asy_tuning(C.Structure):
     _fields_ = [("dense_kernel", C.c_int32), ("panel_park", C.c_int32), ("slab_hold", C.c_int32),
-                ("slab_chunk_rows", C.c_int32), ("slab_ring", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("slab_chunk_rows", C.c_int32), ("slab_ring", C.c_int32), ("measure_delay", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 class asy_solve_params(C.Structure):
@@ -83,7 +84,8 @@ _lib.asy_solve.argtypes = [_H, C.POINTER(asy_solve_params), C.POINTER(asy_solve_
 _lib.asy_stationarity.argtypes = [_H, _vp, C.c_int32, C.POINTER(asy_stationarity_out)]
 _lib.asy_get_x.argtypes = [_H, _vp, C.c_int32]
 _lib.asy_objective.argtypes = [_H, _dp]
-_lib.asy_get_residual.argtypes = [_H, _vp, C.c_int32]
+if hasattr(_lib, "asy_get_residual") or not os.environ.get("ASY_LIB_VARIANT"):  # (older developer builds lack it)
+    _lib.asy_get_residual.argtypes = [_H, _vp, C.c_int32]
 _lib.asy_last_error.argtypes = [_H]
 _lib.asy_last_error.restype = C.c_char_p
 _lib.asy_version.restype = C.c_char_p

@@ -74,7 +74,7 @@ struct asy_handle {
     int64_t gemv_chunks = 1, gemv_cpc = 1;
     Dev red_part, red_out;                // reduction buffers
     // async state
-    Dev counter, gacc, dpart, arrive, consumed, done, ver;
+    Dev counter, gacc, dpart, arrive, consumed, done, ver, wcnt;
     Dev dobs;                             // observed-delay statistic (u32)
     int64_t slots = 0;
     int64_t epochs = 0;                   // sweeps since reset (schedule epoch)
@@ -160,7 +160,7 @@ static void free_problem(asy_handle* h) {
     Dev* all[] = {&h->A, &h->colptr, &h->rowidx, &h->vals, &h->rowptr, &h->csr_col, &h->csr_val, &h->b,
                   &h->tau, &h->lo, &h->hi, &h->x, &h->xalt, &h->r, &h->dx, &h->w, &h->mf, &h->mer, &h->rs, &h->xs,
                   &h->part, &h->gacc, &h->dpart, &h->arrive, &h->consumed, &h->done,
-                  &h->ver, &h->dobs};
+                  &h->ver, &h->dobs, &h->wcnt};
     for (Dev* d : all) dev_free(*d);
     h->has_problem = false;
 }
@@ -659,6 +659,9 @@ static int dense_geometry(asy_handle* h, const asy_solve_params* sp, int64_t del
     return ASY_OK;
 }
 
+#ifndef ASY_LGW_MAX
+#define ASY_LGW_MAX 3  // D1 windows of at most 8 sequences
+#endif
 static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t sweeps, int64_t delay,
                               float* ms, bool* too_tall) {
     DenseGeom geo;
@@ -686,6 +689,15 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     TRY(dev_alloc(h, h->arrive, sizeof(unsigned) * slots * kCtrPad));
     TRY(dev_alloc(h, h->consumed, sizeof(unsigned) * slots * kCtrPad));
     TRY(dev_alloc(h, h->ver, sizeof(unsigned) * h->nblk * kCtrPad));
+    // D1 windows: W <= delay + 1 sequences (the windows a sequence waits for end before it),
+    // SW > (delay + 2) / W + 2 slots (a window slot is reused only after its window completed)
+    const int64_t geo_delay = geo.delay;
+    int lg_w = 0;
+    while (lg_w < ASY_LGW_MAX && ((int64_t)2 << lg_w) <= (geo_delay + 1) / 4) ++lg_w;  // (W <= (delay + 1) / 4)
+    const int64_t wslots = next_pow2(std::max<int64_t>(64, ((geo_delay + 2) >> lg_w) + 8));
+    int lg_sw = 0;
+    while (((int64_t)1 << lg_sw) < wslots) ++lg_sw;
+    TRY(dev_alloc(h, h->wcnt, sizeof(unsigned) * wslots * kCtrPad));
 
     DenseAsyncParams P{};
     P.A = P_<double>(h->A); P.lda = h->lda;
@@ -694,6 +706,10 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk; P.R = R; P.G = G; P.use_tmem = geo.use_tmem;
     // claims of 2 subtasks for narrow blocks (measured +4% on configs[1]), 4 otherwise (configs[2])
     P.claim = geo.Bpad <= 32 ? 2 : kClaim;
+    // cyclic schedule with delay < N - 1: a block's previous update (sequence k - N) is covered by
+    // the D1 watermark's acquire; otherwise the D4 loads acquire themselves
+    P.wcnt = P_<unsigned>(h->wcnt); P.lg_w = lg_w; P.lg_sw = lg_sw;
+    P.measure_delay = tuning_of(sp).measure_delay != 0;
     if (const char* e = dbg_env("ASY_CLAIM_N")) P.claim = std::max(1, std::min(kClaim, atoi(e)));
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
     P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
@@ -737,7 +753,7 @@ static int dense_async_launch(asy_handle* h, const asy_solve_params* sp, int64_t
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
-    {
+    if (P.measure_delay) {
         unsigned dobs = 0;
         CK(cudaMemcpy(&dobs, h->dobs.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
         h->last_dobs = std::max(h->last_dobs, (int)dobs);
@@ -1148,6 +1164,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     P.epoch0 = h->epochs; P.T = sweeps * NB; P.NB = NB; P.BS = BS; P.delay = delay;
     P.counter = P_<unsigned long long>(h->counter);
     P.ver = P_<unsigned>(h->ver); P.wcnt = P_<unsigned>(h->done); P.lgW = lgW; P.lgS = lgS;
+    P.measure_delay = tuning_of(sp).measure_delay != 0;
     P.dobs = P_<unsigned>(h->dobs);
     h->last_kernel = ASY_KERNEL_SPARSE;
     h->last_delay = (int)delay;
@@ -1165,7 +1182,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     CK(cudaEventSynchronize(h->ev[1]));
     CKL();
     CK(cudaEventElapsedTime(ms, h->ev[0], h->ev[1]));
-    {
+    if (P.measure_delay) {
         unsigned dobs = 0;
         CK(cudaMemcpy(&dobs, h->dobs.p, sizeof(unsigned), cudaMemcpyDeviceToHost));
         h->last_dobs = std::max(h->last_dobs, (int)dobs);
@@ -1191,7 +1208,8 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
         if ((t.dense_kernel != 0 && t.dense_kernel != ASY_KERNEL_DENSE_PANEL && t.dense_kernel != ASY_KERNEL_DENSE_SLAB &&
              t.dense_kernel != ASY_KERNEL_DENSE_SLAB_TMEM) ||
             (t.panel_park != 0 && t.panel_park != 2) || t.slab_hold < 0 || t.slab_hold > 2 || t.slab_chunk_rows < 0 ||
-            t.slab_chunk_rows > 256 || t.slab_ring < 0 || t.slab_ring > 16)
+            t.slab_chunk_rows > 256 || t.slab_ring < 0 || t.slab_ring > 16 || t.measure_delay < 0 ||
+            t.measure_delay > 1)
             return h->fail(ASY_ERR_INVALID, "bad asy_tuning field");
     }
     CK(cudaSetDevice(h->device));

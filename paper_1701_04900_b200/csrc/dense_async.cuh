@@ -47,12 +47,14 @@
 //   * D4 freshness [PAPER.md:233]: block b is not read before its previous
 //     update is complete -- applied to r and written to x (xver[b] = u*G);
 //   * bounded delay D1 [PAPER.md:224]: sequence k does not read before EVERY
-//     sequence up to k - delay - 1 is complete.  Each scheduler keeps an in-order
-//     watermark wm (all sequences < wm complete) and advances it over the completion
-//     counters in sequence order, so sequences finishing out of order across CTAs never
-//     let a read run more than delay updates ahead of the oldest missing one;
-//   * slot reuse: sequence k - S (previous user of the slot) is complete -- implied by
-//     the watermark (S > delay + 1).
+//     sequence up to k - delay - 1 is complete.  Sequences are grouped in windows of W
+//     consecutive sequences; every completed panel adds 1 to its window's counter
+//     (wcnt[w mod SW], monotone), so window w is complete when it holds (w / SW + 1) W G.
+//     The scheduler keeps its count of leading complete windows and admits sequence k only
+//     when every window holding a sequence <= k - delay - 1 is complete (one counter load
+//     per W sequences; W <= delay + 1 keeps those windows older than k);
+//   * slot reuse: sequence k - S (previous user of the slot) is complete -- implied by D1
+//     (S > delay + 1).
 // delay == 0 makes the kernel the sequential (d^k = 0) scheme and, with the
 // fixed-order partial reduction (deterministic = 1), bit-reproducible.
 #pragma once
@@ -82,11 +84,11 @@ constexpr int kRoll = ASY_ROLL;
 #ifndef ASY_CLAIM
 #define ASY_CLAIM 4  // most subtasks claimed per atomic (runtime: DenseAsyncParams::claim)
 #endif
-#ifndef ASY_PROXY_FENCE
-#define ASY_PROXY_FENCE 1
+#ifndef ASY_SCHED_DUMMY
+#define ASY_SCHED_DUMMY 0
 #endif
 constexpr int kQueue = ASY_QUEUE;    // scheduler -> producer queue depth
-constexpr int kWm = 8;               // completion counters loaded per batch past the D1 watermark
+constexpr int kWs = 4;               // D1 window counters a sampling batch loads at once
 constexpr int kRing = 32;            // hand-off notes per axpy warp
 constexpr int kMaxRowsPerLane = 8;   // R <= 256 (one TMA box per panel)
 constexpr int kClaim = ASY_CLAIM;    // subtasks claimed per atomic
@@ -139,8 +141,11 @@ struct DenseAsyncParams {
     int lg_slots;        // log2(slots)
     int32_t Bmax;        // = B
     int32_t Bpad;        // B rounded up to 8 (TMEM row layout)
-    unsigned* dobs;             // observed delay: max over admitted subtasks of k - (first sequence
-                                // not known complete), an upper bound on d^k of Assumption D1
+    unsigned* wcnt;      // [SW]       monotonic: completed panels of the windows using the slot (D1)
+    int lg_w;            // log2 W (sequences per window)
+    int lg_sw;           // log2 SW (window slots)
+    int measure_delay;   // sample the observed delay (costs scheduler stalls; asy_tuning.measure_delay)
+    unsigned* dobs;      // observed delay: max over sampled admissions of k - W * (leading complete windows)
     unsigned long long* prof;   // optional [grid][warps][8] clock64 segment sums (debug; null = off)
     unsigned long long* trace;  // optional [trace_n][8] globaltimer stamps (debug; null = off)
     int64_t trace_n;
@@ -205,6 +210,7 @@ __global__ void dense_async_init(DenseAsyncParams P) {
     }
     for (int64_t i = tid; i < 2 * P.slots * kPanelRep * P.Bmax; i += nth) P.gacc[i] = 0.0;
     for (int64_t i = tid; i < P.nblk; i += nth) P.xver[i * kCtrPad] = 0u;
+    for (int64_t i = tid; i < ((int64_t)1 << P.lg_sw); i += nth) P.wcnt[i * kCtrPad] = 0u;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
@@ -422,11 +428,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const long long nr = (P.m - r0) < R ? (P.m - r0) : R;
                 const uint32_t rbytes = (uint32_t)(((nr + 1) & ~1ll) * 8);
                 double* dst = stages + st * STAGE;
-#if ASY_PROXY_FENCE
-                // the residual rows were updated by other SMs' red.adds (generic proxy) and are read
-                // by the bulk copy (async proxy): order the scheduler's acquire before the copy
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-#endif
                 mbar_arrive_expect_tx(&full[st], box_bytes + 2 * rbytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
                 bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
@@ -449,18 +450,25 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             // permutation keys once per epoch), check the guards, queue them.  The next claim's
             // atomic is issued before this batch is processed so its round trip overlaps.
             const long long G = P.G, N = P.nblk;
-            const int lgS = P.lg_slots;
+            const int lgW = P.lg_w, lgSW = P.lg_sw;
+            const long long swmask = (1ll << lgSW) - 1;
+            const unsigned WG = (unsigned)G << lgW;  // completed panels of a window
+            // window w complete: its slot holds (w / SW + 1) W G completions
+            auto wneed = [&](long long w) { return (unsigned)((w >> lgSW) + 1) * WG; };
+            long long wdone = 0;  // leading complete windows (every sequence < W wdone complete)
+            long long dmax = 0;   // observed delay (sampled)
+            unsigned nbatch = 0;
+            bool sample = false;
             const int half = perm_half_bits(N);
-            PermKeys pk{};
-            long long ck = -1, cb = 0, cu = 0, cE = -1;  // cached sequence / block / epochs
-            long long wm = 0;    // in-order watermark: every sequence < wm is complete
-            long long dmax = 0;  // observed delay (max k - wm at admission)
+            PermKeys pk{}, pkp{};
+            long long ck = -1, cb = 0, cu = 0, cE = -1, cprev = -1;  // cached sequence / block / epochs
             const int nclaim = P.claim;
             long long tb = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
             while (tb < P.T) {
                 const long long tn = (long long)atomicAdd(P.counter, (unsigned long long)nclaim);
                 StageMeta e[kClaim];
                 unsigned xv[kClaim];
+                long long kprev[kClaim];
                 long long k = tb / G, p = tb - k * G;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
@@ -474,12 +482,23 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                         cu = k / N;
                         const long long pos = k - cu * N;
                         cb = pos;
+                        cprev = k - N;  // the block's previous update (cyclic: one epoch earlier)
                         if (P.sched == SCHED_RANDOM) {
                             const long long E = P.epoch0 + cu;
-                            if (E != cE) { pk = perm_keys(P.seed, E); cE = E; }
+                            if (E != cE) {
+                                pk = perm_keys(P.seed, E);
+                                if (E > 0) pkp = perm_keys(P.seed, E - 1);
+                                cE = E;
+                            }
                             uint64_t v = (uint64_t)pos;
                             do { v = feistel(v, half, pk); } while (v >= (uint64_t)N);
                             cb = (long long)v;
+                            // its position in the previous epoch (inverse permutation, cycle-walking)
+                            if (E > 0) {
+                                uint64_t w = v;
+                                do { w = feistel_inv(w, half, pkp); } while (w >= (uint64_t)N);
+                                cprev = (cu - 1) * N + (long long)w;
+                            }
                         }
                     }
                     e[i].t = t < P.T ? t : -1;
@@ -487,57 +506,87 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     e[i].p = p;
                     e[i].b = cb;
                     e[i].u = cu;
+                    kprev[i] = cprev;
                     ASY_TRACE(P, t, 0);
                     if (++p == G) { p = 0; ++k; }
                 }
-                // guards: all loads in flight at once -- block freshness (D4) per subtask and the
-                // completion counters of the next kWm sequences past the watermark (D1, slot reuse)
+                // guards.  D1 needs a window counter load only when the bound moves into a window not
+                // yet known complete (once per W sequences); every 16th batch looks up to kWs windows
+                // ahead so that the observed delay tracks the real lag.  D4 (the block's previous
+                // update complete) is implied by D1 when that update lies in a complete window --
+                // always for the cyclic schedule with delay < N - W -- and loaded otherwise.
                 long long kdmax = -1;
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i)
                     if (e[i].t >= 0) kdmax = e[i].k - P.delay - 1;
-                unsigned cwl[kWm];
+                const long long nwmax = kdmax >= 0 ? (kdmax + (1ll << lgW)) >> lgW : 0;  // windows needed
+                // observed delay (measurement mode only, asy_tuning.measure_delay): every 16th batch
+                // loads the counters of the next kWs windows and advances the count of complete
+                // windows over them.  Off by default: those counters sit on lines under heavy atomic
+                // traffic and the scheduler would stall on them (measured 9% on configs[1]).
+                if (P.measure_delay && (++nbatch & 15) == 0) {
+                    unsigned wcs[kWs];
 #pragma unroll
-                for (int u = 0; u < kWm; ++u) {
-                    const long long sq = wm + u;
-                    cwl[u] = sq <= kdmax ? ld_relaxed_u32(&P.consumed[(sq & (P.slots - 1)) * kCtrPad]) : 0u;
-                }
-#pragma unroll
-                for (int i = 0; i < kClaim; ++i)
-                    xv[i] = e[i].t >= 0 ? ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]) : 0u;
-                // advance the watermark over the sequences already complete, in order
-                {
+                    for (int u = 0; u < kWs; ++u) wcs[u] = ld_relaxed_u32(&P.wcnt[((wdone + u) & swmask) * kCtrPad]);
                     bool run = true;
 #pragma unroll
-                    for (int u = 0; u < kWm; ++u) {
-                        const long long sq = wm;
-                        run = run && sq <= kdmax && cwl[u] >= (unsigned)((sq >> lgS) + 1) * (unsigned)G;
-                        if (run) ++wm;
+                    for (int u = 0; u < kWs; ++u) {
+                        run = run && wcs[u] >= wneed(wdone);
+                        if (run) ++wdone;
                     }
+                    sample = true;
                 }
+                // D1 needs one more window: one (blocking) load, once per W sequences
+                unsigned wc = 0u;
+                if (wdone < nwmax) wc = ld_relaxed_u32(&P.wcnt[(wdone & swmask) * kCtrPad]);
+#pragma unroll
+                for (int i = 0; i < kClaim; ++i) {
+                    xv[i] = 0u;
+                    if (e[i].t >= 0 && kprev[i] >= (wdone << lgW))
+                        xv[i] = ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]);
+                }
+                if (wdone < nwmax && wc >= wneed(wdone)) ++wdone;
+#if ASY_SCHED_DUMMY
+                {   // (measurement: the round-1 scheduler's per-batch counter loads, values unused)
+                    unsigned dsum = 0;
+#pragma unroll
+                    for (int i = 0; i < kClaim; ++i) {
+                        if (e[i].t < 0) continue;
+                        const long long kk = e[i].k, kd = kk - P.delay - 1;
+                        dsum += ld_relaxed_u32(&P.xver[e[i].b * kCtrPad]);
+                        dsum += ld_relaxed_u32(&P.consumed[(kk & (P.slots - 1)) * kCtrPad]);
+                        if (kd >= 0) dsum += ld_relaxed_u32(&P.consumed[(kd & (P.slots - 1)) * kCtrPad]);
+                    }
+                    if (dsum == 0xFFFFFFFFu) wdone = 0;
+                }
+#endif
                 // admit in claim order: a subtask never waits while an older one of this batch is
-                // held back.  Polls are relaxed (ld.acquire would invalidate the SM's L1 on every
-                // poll); one fence per batch then orders the admitted reads after the observed
-                // completions (acquire), before the producer's bulk copies read r.
-                bool waited = false;
+                // held back.  Guards are observed with relaxed loads and a fence follows only a guard
+                // that had to wait: the counters were released (fence + red) by the SMs that completed
+                // the updates, and what an admitted subtask reads that they wrote -- residual rows (bulk
+                // copy), x and the accumulator (ld.relaxed.gpu) -- is read from L2, never through L1.
+                // (A fence or ld.acquire on every admission measured 10-14% slower.)
 #pragma unroll
                 for (int i = 0; i < kClaim; ++i) {
                     if (e[i].t < 0) continue;
                     const long long kk = e[i].k, kd = kk - P.delay - 1;
-                    while (wm <= kd) {  // D1: every sequence up to kd complete
-                        spin_until_ge_relaxed(&P.consumed[(wm & (P.slots - 1)) * kCtrPad],
-                                              (unsigned)((wm >> lgS) + 1) * (unsigned)G);
-                        ++wm;
+                    const long long nw = kd >= 0 ? (kd + (1ll << lgW)) >> lgW : 0;
+                    bool waited = false;
+                    while (wdone < nw) {  // D1: every window holding a sequence <= kd complete
+                        spin_until_ge_relaxed(&P.wcnt[(wdone & swmask) * kCtrPad], wneed(wdone));
+                        ++wdone;
                         waited = true;
                     }
-                    const unsigned need_x = (unsigned)e[i].u * (unsigned)G;  // previous update of b (D4)
-                    if (xv[i] < need_x) {
-                        spin_until_ge_relaxed(&P.xver[e[i].b * kCtrPad], need_x);
-                        waited = true;
+                    if (kprev[i] >= (wdone << lgW)) {  // D4 not implied by D1
+                        const unsigned need_x = (unsigned)e[i].u * (unsigned)G;
+                        if (xv[i] < need_x) {
+                            spin_until_ge_relaxed(&P.xver[e[i].b * kCtrPad], need_x);
+                            waited = true;
+                        }
                     }
-                    if (kk - wm > dmax) dmax = kk - wm;
-                    if (i == 0 || waited) fence_acqrel_gpu();
-                    waited = false;
+                    if (waited) fence_acqrel_gpu();
+                    if (sample && i == 0 && kk - (wdone << lgW) > dmax) dmax = kk - (wdone << lgW);
+                    if (i == 0) sample = false;
                     push(e[i]);
                 }
                 tb = tn;
@@ -707,12 +756,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         uint64_t* myfull = rfull + ax * kRing;
         uint64_t* myempty = rempty + ax * kRing;
         unsigned tm_fin = 0;
-        long long pend_slot = -1, pend_b = -1;  // completion of the previous panel, issued late
+        long long pend_slot = -1, pend_b = -1, pend_k = 0;  // completion of the previous panel, issued late
         auto complete = [&]() {
             if (pend_slot >= 0 && lane == 0) {
                 fence_acqrel_gpu();  // r red.adds, x / accumulator writes before the counts (one membar)
                 red_add_u32(&P.consumed[pend_slot * kCtrPad], 1u);
                 red_add_u32(&P.xver[pend_b * kCtrPad], 1u);
+                red_add_u32(&P.wcnt[((pend_k >> P.lg_w) & ((1ll << P.lg_sw) - 1)) * kCtrPad], 1u);
             }
             pend_slot = -1;
         };
@@ -875,6 +925,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             ASY_TRACE(P, md.t, 7);
             pend_slot = slot;
             pend_b = b;
+            pend_k = k;
             sp.mark(5);
         }
         complete();

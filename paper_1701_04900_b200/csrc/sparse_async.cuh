@@ -58,11 +58,17 @@ struct SparseAsyncParams {
     int lgW;                      // W = 2^lgW batches per window
     int lgS;                      // S = 2^lgS window slots
     unsigned* dobs;               // observed delay (max)
+    int measure_delay;            // sample the observed delay (asy_tuning.measure_delay)
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32_g(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32_g(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ long long ld_relaxed_s64_g(const long long* p) {
@@ -119,7 +125,11 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
 #ifndef ASY_SPARSE_CH
 #define ASY_SPARSE_CH 8  // nonzeros per lane held in registers (longer columns loop over the rest)
 #endif
+#ifndef ASY_SPARSE_CLAIM
+#define ASY_SPARSE_CLAIM 1  // batches claimed per atomic
+#endif
 constexpr int kSparseThreads = ASY_SPARSE_THREADS;
+constexpr int kSparseClaim = ASY_SPARSE_CLAIM;
 constexpr int kSparseCh = ASY_SPARSE_CH;
 
 // LPC lanes per column (1, 2, 4 or 8): batch lanes b = lane / LPC, element lane e = lane % LPC.
@@ -139,11 +149,13 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
     int64_t pkE = -1;
     unsigned dmax = 0;
 
-    // the head of a batch's update for this lane: sequence, block, column extent, x / tau / ver
+    // the head of a batch's update for this lane: sequence, block, column extent, tau, ver.
+    // ver is read with ld.acquire: when it shows the block's previous update applied (D4), every
+    // later read of this warp sees that update's writes.
     struct Head {
-        long long t;      // batch (-1: none)
+        long long t;      // batch
         int64_t e, k, j;  // epoch (local), sequence (local), block = column
-        int64_t s, c;     // column start, nonzero count
+        int64_t s, s1;    // column extent [s, s1)
         bool live;        // this lane's update exists
         unsigned vj;
         double tj;
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
         const int64_t i = i0 + bl;
         h.live = t < P.T && bl < BS && i < N;
         h.k = h.e * N + i;
-        h.j = 0; h.s = 0; h.c = 0; h.vj = 0; h.tj = 1.0;
+        h.j = 0; h.s = 0; h.s1 = 0; h.vj = 0; h.tj = 1.0;
         if (h.live) {
             h.j = i;
             if (P.sched == SCHED_RANDOM) {
@@ -167,98 +179,115 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
                 h.j = (int64_t)v;
             }
             h.s = __ldg(&P.colptr[h.j]);
-            h.c = __ldg(&P.colptr[h.j + 1]) - h.s;
+            h.s1 = __ldg(&P.colptr[h.j + 1]);
             if (el == 0) {
-                h.vj = ld_relaxed_u32_g(&P.ver[h.j]);
+                h.vj = ld_acquire_u32_g(&P.ver[h.j]);
                 h.tj = __ldg(&P.tau[h.j]);
             }
         }
         return h;
     };
-    auto claim = [&]() {
-        long long t = 0;
-        if (lane == 0) t = (long long)atomicAdd(P.counter, 1ull);
-        return __shfl_sync(0xffffffffu, t, 0);
-    };
     auto kfirst = [&](long long t) { const int64_t e = t / NB; return e * N + (t - e * NB) * (int64_t)BS; };
     // batch containing sequence k (local numbering)
     auto batch_of = [&](long long k) { const int64_t e = k / N; return e * NB + (k - e * N) / BS; };
 
-    // completion of batch t (after its scatter): fence (the batch's r red.adds and x stores
-    // first), per-block versions, and one count on the batch's window
+    // Completion of a batch: fence (every lane's r red.adds and x store of the batch first), then
+    // the per-block versions and one count on the batch's window.  It is issued one iteration
+    // late -- after the next batch's gathers, when the batch's writes have long reached L2 and
+    // the fence costs little -- except that a warp never waits in a guard while holding one.
     long long pend = -1;
     int64_t pend_j = 0;
     bool pend_live = false;
-    auto complete = [&]() {
+    auto release = [&]() {
         if (pend < 0) return;
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // every lane: its own atomics / x store
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
         if (pend_live && el == 0) red_relaxed_u32_g(&P.ver[pend_j], 1u);
         if (lane == 0) red_relaxed_u32_g(&P.wcnt[(pend >> lgW) & Smask], 1u);
         pend = -1;
     };
 
-    long long t = claim();
-    Head nx = head(t);
-    while (nx.t < P.T) {
-        const Head cur = nx;
-        // previous batch's completion (its fence also waits for this head's loads)
-        complete();
-        // D1: every window holding a batch up to batch(k_max - delta - 1) complete
-        {
-            const int64_t i0 = (cur.t - cur.e * NB) * (int64_t)BS;
-            const int64_t nlive = (N - i0) < BS ? (N - i0) : BS;
-            const long long kmax = cur.e * N + i0 + nlive - 1;
-            const long long kd = kmax - P.delay - 1;
-            // every 32nd batch of a warp refreshes its window count even when the guard holds (the
-            // observed delay below is then the real lag of the residual, not of a stale count)
-            const long long nw = kd >= 0 ? (batch_of(kd) + (1ll << lgW)) >> lgW : 0;  // windows needed
-            const bool sample = (++iter & 31) == 0;
-            if (wmw < nw || sample) {
-                unsigned ns = 32;
-                for (;;) {
-                    // lane l: is window wmw + l complete?
-                    const long long w = wmw + lane;
-                    const unsigned c = ld_relaxed_u32_g(&P.wcnt[w & Smask]);
-                    const bool ok = c >= (unsigned)(((w >> lgS) + 1) << lgW);
-                    const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                    wmw += bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
-                    if (bal == 0xffffffffu) continue;  // maybe more complete windows
-                    if (wmw >= nw) break;
-                    __nanosleep(ns);
-                    if (ns < 256) ns <<= 1;
-                }
-            }
-            // observed delay: sequences before batch W * wmw are all applied
-            if (sample && cur.live && el == 0) {
-                const long long miss = cur.k - kfirst(wmw << lgW);
-                if (miss > (long long)dmax) dmax = (unsigned)miss;
+    // claims run one batch ahead: the atomic for the batch after the next one is in flight
+    // while the current batch runs; each atomic claims kSparseClaim consecutive batches
+    long long t0 = 0;
+    if (lane == 0) t0 = (long long)atomicAdd(P.counter, (unsigned long long)kSparseClaim);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    Head cur = head(t0);
+    long long cbase = t0;
+    int cused = 1;
+    unsigned long long cl = 0;
+    if (kSparseClaim == 1 && lane == 0) cl = atomicAdd(P.counter, 1ull);
+    while (cur.t < P.T) {
+        long long tn;
+        if (kSparseClaim == 1) {
+            tn = __shfl_sync(0xffffffffu, (long long)cl, 0);
+            if (lane == 0) cl = atomicAdd(P.counter, 1ull);
+        } else {
+            if (cused == kSparseClaim) {
+                tn = __shfl_sync(0xffffffffu, (long long)cl, 0);
+                cbase = tn;
+                cused = 1;
+            } else {
+                tn = cbase + cused++;
+                // the next claim goes out with the group's last batch
+                if (cused == kSparseClaim && lane == 0) cl = atomicAdd(P.counter, (unsigned long long)kSparseClaim);
             }
         }
+        const Head nx = head(tn);
+        // D1: every window holding a batch up to batch(k_max - delta - 1) complete
+        const int64_t i0 = (cur.t - cur.e * NB) * (int64_t)BS;
+        const int64_t nlive = (N - i0) < BS ? (N - i0) : BS;
+        const long long kd = cur.e * N + i0 + nlive - 1 - P.delay - 1;
+        const long long nw = kd >= 0 ? (batch_of(kd) + (1ll << lgW)) >> lgW : 0;  // windows needed
         // D4: the previous update of this block applied
-        if (cur.live && el == 0 && cur.vj < (unsigned)cur.e) {
+        const bool d4 = cur.live && el == 0 && cur.vj < (unsigned)cur.e;
+        const bool d4any = __any_sync(0xffffffffu, d4);
+        if (wmw < nw || d4any) release();
+        // every 32nd batch of a warp refreshes its window count even when the guard holds (the
+        // observed delay below is then the real lag of the residual, not of a stale count)
+        const bool sample = P.measure_delay && (++iter & 31) == 0;
+        if (wmw < nw || sample) {
             unsigned ns = 32;
-            while (ld_relaxed_u32_g(&P.ver[cur.j]) < (unsigned)cur.e) {
+            for (;;) {
+                // lane l: is window wmw + l complete?
+                const long long w = wmw + lane;
+                const unsigned c = ld_acquire_u32_g(&P.wcnt[w & Smask]);
+                const bool ok = c >= (unsigned)(((w >> lgS) + 1) << lgW);
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                wmw += bal == 0xffffffffu ? 32 : __ffs(~bal) - 1;
+                if (bal == 0xffffffffu) continue;  // maybe more complete windows
+                if (wmw >= nw) break;
                 __nanosleep(ns);
                 if (ns < 256) ns <<= 1;
             }
         }
-        __syncwarp();
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire (every lane observed a guard)
-        // next batch: claim and load its head while this one runs
-        const long long tn = claim();
-        nx = head(tn);
+        // observed delay: sequences before batch W * wmw are all applied
+        if (sample && cur.live && el == 0) {
+            const long long miss = cur.k - kfirst(wmw << lgW);
+            if (miss > (long long)dmax) dmax = (unsigned)miss;
+        }
+        if (d4) {
+            unsigned ns = 32;
+            while (ld_acquire_u32_g(&P.ver[cur.j]) < (unsigned)cur.e) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+        __syncwarp();  // every lane's reads below are ordered after the guards' acquire loads
+        double d = 0.0, xn = 0.0;
+        int32_t rows[kSparseCh];
+        double vv[kSparseCh];
+        const int64_t cnt = cur.s1 - cur.s;
         if (cur.live) {
             double xj = 0.0;
             if (el == 0) xj = ld_relaxed_f64(&P.x[cur.j]);
             // gradient: sum_q a_qj phi'(r_q) over the column (inconsistent read of r)
-            int32_t rows[kSparseCh];
-            double vv[kSparseCh];
 #pragma unroll
             for (int u = 0; u < kSparseCh; ++u) {
                 const int64_t q = el + (int64_t)u * LPC;
                 rows[u] = 0;
                 vv[u] = 0.0;
-                if (q < cur.c) {
+                if (q < cnt) {
                     rows[u] = __ldg(&P.rowidx[cur.s + q]);
                     vv[u] = __ldg(&P.vals[cur.s + q]);
                 }
@@ -267,41 +296,45 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
 #pragma unroll
             for (int u = 0; u < kSparseCh; ++u) {
                 const int64_t q = el + (int64_t)u * LPC;
-                if (q < cur.c) {
+                if (q < cnt) {
                     const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)rows[u]]);
                     acc = fma(vv[u], loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
                 }
             }
-            for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cur.c; q += LPC) {
+            for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cnt; q += LPC) {
                 const int32_t row = __ldg(&P.rowidx[cur.s + q]);
                 const double2 ra = ld_relaxed_f64x2(&P.r[2 * (int64_t)row]);
                 acc = fma(__ldg(&P.vals[cur.s + q]), loss_prime_t<LOSS>(P.S, ra.x, ra.y), acc);
             }
 #pragma unroll
             for (int o = LPC / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(cmask, acc, o);
-            double d = 0.0;
             if (el == 0) {
                 const double xh = best_response(P.S, acc, xj, cur.tj, cur.j);
-                const double xn = xj + P.gamma * (xh - xj);
-                P.x[cur.j] = xn;
+                xn = xj + P.gamma * (xh - xj);
                 d = xn - xj;
             }
             if (LPC > 1) d = __shfl_sync(cmask, d, bl * LPC);
+        }
+        // the previous batch's completion, then this batch's writes
+        release();
+        if (cur.live) {
+            if (el == 0) P.x[cur.j] = xn;
             if (d != 0.0) {
 #pragma unroll
                 for (int u = 0; u < kSparseCh; ++u) {
                     const int64_t q = el + (int64_t)u * LPC;
-                    if (q < cur.c) red_relaxed_add_f64_g(&P.r[2 * (int64_t)rows[u]], vv[u] * d);
+                    if (q < cnt) red_relaxed_add_f64_g(&P.r[2 * (int64_t)rows[u]], vv[u] * d);
                 }
-                for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cur.c; q += LPC)
+                for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cnt; q += LPC)
                     red_relaxed_add_f64_g(&P.r[2 * (int64_t)__ldg(&P.rowidx[cur.s + q])], __ldg(&P.vals[cur.s + q]) * d);
             }
         }
         pend = cur.t;
         pend_j = cur.j;
         pend_live = cur.live;
+        cur = nx;
     }
-    complete();
+    release();
     // warp max of the observed delay, one atomic per warp
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {

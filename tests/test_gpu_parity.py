@@ -483,3 +483,28 @@ def test_panel_kernel_too_many_panels_never_hangs(A):
         assert _rel_x(S.x(), x_or) <= REL
     finally:
         S.close()
+
+
+@pytest.mark.parametrize("case,schedule", [("config0", "cyclic"), ("dense_ragged", "random"), ("large_block", "cyclic"),
+                                           ("sparse_logistic", "cyclic"), ("sparse_ls", "random")])
+def test_observed_delay_panel_and_csc(A, case, schedule):
+    """Observed delay (Assumption D1's d^k [PAPER.md:224]) of the panel and CSC kernels in
+    measurement mode (asy_tuning.measure_delay): 0 in sequential mode, within the enforced bound
+    otherwise, and not measured (-1) by default; the measurement does not change the iterates
+    of the sequential mode."""
+    P = make_case(case)
+    S = A.Solver(P)
+    sched = A.ASY_SCHED_CYCLIC if schedule == "cyclic" else A.ASY_SCHED_RANDOM
+    T = {"dense_kernel": A.ASY_KERNEL_DENSE_PANEL} if P.kind == "dense" else {}
+    try:
+        st = S.solve(sweeps=2, max_delay=0, reset=True, schedule=sched, seed=5, tuning=dict(T, measure_delay=1))
+        assert st.kernel in (A.ASY_KERNEL_DENSE_PANEL, A.ASY_KERNEL_SPARSE)
+        assert st.delay_observed == 0
+        x_meas = S.x()
+        st = S.solve(sweeps=2, max_delay=0, reset=True, schedule=sched, seed=5, tuning=T or None)
+        assert st.delay_observed == -1
+        assert np.array_equal(S.x(), x_meas)
+        st = S.solve(sweeps=20, reset=True, schedule=sched, seed=5, tuning=dict(T, measure_delay=1))
+        assert 0 <= st.delay_observed <= st.delay
+    finally:
+        S.close()
