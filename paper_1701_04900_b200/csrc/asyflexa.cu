@@ -840,7 +840,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     if ((nrg + kSlabDot - 1) / kSlabDot > kSlabTMaxG) return false;
     const size_t unit = sizeof(double) * 32 * 16, hslot = sizeof(double) * 32 * CS;
     const int64_t RsP = (Rs + 1) & ~1ll;
-    const size_t fixed = sizeof(double) * (3 * RsP + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
+    const size_t fixed = sizeof(double) * (3 * RsP + kSlabDot * kSlabTMaxG * 32 + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
                          (sizeof(SeqMeta) + sizeof(long long)) * kSlabNM +
                          sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 3 * kSlabNDX) +
                          sizeof(unsigned long long) * (kSlabAx + kSlabDot) + sizeof(unsigned) * (kSlabDot + 1) + 256;

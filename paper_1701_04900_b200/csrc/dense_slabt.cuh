@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     double* rs = hold + (size_t)P.nsa * HSLOT;                        // Rs   residual slab
     double* auxs = rs + RsP;                                          // Rs   b / y slab
     double* delta = auxs + RsP;                                       // Rs   pending sub-sequence axpy
-    double* pring = delta + RsP;                                      // NP * kSlabDot * CS
+    double* wscr = delta + RsP;                                       // kSlabDot * kSlabTMaxG * 32: w = phi'(r) per dot warp
+    double* pring = wscr + kSlabDot * kSlabTMaxG * 32;                // NP * kSlabDot * CS
     double* dxring = pring + kSlabNP * kSlabDot * CS;                 // NDX * CS
     SeqMeta* meta = reinterpret_cast<SeqMeta*>(dxring + kSlabNDX * CS);  // NM
     long long* meta_k = reinterpret_cast<long long*>(meta + kSlabNM);    // NM ready flags
@@ -292,8 +293,15 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         unsigned used = 0;  // park slots taken
         int pslot = 0;      // used mod np
         long long dmax_local = 0;
+        // Lane layout of a 32 x 16 unit (see the header): lane (co = lane >> 2, rq = lane & 3)
+        // owns columns 2 co, 2 co + 1 and the row pairs rq + 4 (j ^ (co & 1)), j < 4, read as
+        // double2 (8 conflict-free 16-byte loads per unit); the sum over rows is then in-lane
+        // except for the four rq lanes (two shuffles per 16-column block).
+        const int rq = lane & 3, co = lane >> 2;
+        const int lbase = 64 * co + 2 * rq;                       // doubles: column 2 co, row 2 rq
+        const int o0 = 8 * (co & 1), o1 = 8 - o0;                 // row-pair offsets of j = 0, 1 (j = 2, 3: + 16)
+        double* mywscr = wscr + d * kSlabTMaxG * 32;
         for (int64_t k = 0; k < K; ++k) {
-            double w[kSlabTMaxG];
             const int cnt = cnt_of(d, k);  // my row groups in sequence k
             const int ex = extra_of(d, k);
             if (cnt > 0) {
@@ -328,12 +336,14 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                     if (miss > dmax_local) dmax_local = miss;
                 }
                 sp.mark(1);
-                // one residual snapshot for the whole block update
-#pragma unroll
-                for (int i = 0; i < kSlabTMaxG; ++i) {
-                    const int srow = i < cnt ? 32 * grp_of(d, k, i) + lane : rows;
-                    w[i] = srow < rows ? loss_prime_t<LOSS>(P.S, rs[srow], auxs[srow]) : 0.0;
+                // one residual snapshot for the whole block update (lane = row here; the dot pass
+                // reads it back per row pair)
+                __syncwarp();
+                for (int i = 0; i < cnt; ++i) {
+                    const int srow = 32 * grp_of(d, k, i) + lane;
+                    mywscr[i * 32 + lane] = srow < rows ? loss_prime_t<LOSS>(P.S, rs[srow], auxs[srow]) : 0.0;
                 }
+                __syncwarp();
             }
 #pragma unroll 1
             for (int h = 0; h < NSPLIT; ++h) {
@@ -351,43 +361,65 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                     sp.mark(5);
 #pragma unroll 1
                     for (int cb = 0; cb < ncb; ++cb) {
-                        double acc[16];
-#pragma unroll
-                        for (int c = 0; c < 16; ++c) acc[c] = 0.0;
+                        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;  // columns 2 co (x, y rows), 2 co + 1
 #pragma unroll 1
                         for (int i = 0; i < cnt; ++i) {
-                            {
-                                const double wi = i == 0 ? w[0] : i == 1 ? w[1] : i == 2 ? w[2] : w[3];
-                                const int st = cr.i;
-                                sp.mark(3);
-                                mbar_wait(&myfull[st], cr.ph);
-                                sp.mark(6);
-                                const double* a = mystage + (size_t)st * UNIT + lane;
-                                double v[16];
+                            const int st = cr.i;
+                            sp.mark(3);
+                            mbar_wait(&myfull[st], cr.ph);
+                            sp.mark(6);
+                            const double* a = mystage + (size_t)st * UNIT + lbase;
+                            const double* wp = mywscr + i * 32 + 2 * rq;
+                            double2 wv[4];
+                            wv[0] = *reinterpret_cast<const double2*>(wp + o0);
+                            wv[1] = *reinterpret_cast<const double2*>(wp + o1);
+                            wv[2] = *reinterpret_cast<const double2*>(wp + 16 + o0);
+                            wv[3] = *reinterpret_cast<const double2*>(wp + 16 + o1);
+                            double v[16];  // v[8 cc + 2 j + t] = A[row 2 (rq + 4 (j ^ par)) + t][column 2 co + cc]
 #pragma unroll
-                                for (int c = 0; c < 16; ++c) v[c] = a[c * 32];
-#pragma unroll
-                                for (int c = 0; c < 16; ++c) acc[c] = fma(v[c], wi, acc[c]);
-                                int ps = pslot + i;
-                                if (ps >= np) ps -= np;
-                                if (ps < SQ) {
-                                    const uint32_t t = tq + (uint32_t)(ps * 2 * CS + 2 * 16 * cb);
-                                    tmem_st8(t, v);
-                                    tmem_st8(t + 16, v + 8);
-                                } else {
-                                    double* hp = myhold + (size_t)(ps - SQ) * HSLOT + cb * 16 * 32 + lane;
-#pragma unroll
-                                    for (int c = 0; c < 16; ++c) hp[c * 32] = v[c];
-                                }
-                                sp.mark(2);
-                                __syncwarp();       // every lane's reads of the stage are done
-                                if (lane == 0) mbar_arrive(&myempty[st]);
-                                cr.next();
+                            for (int cc = 0; cc < 2; ++cc) {
+                                const double2 t0 = *reinterpret_cast<const double2*>(a + 32 * cc + o0);
+                                const double2 t1 = *reinterpret_cast<const double2*>(a + 32 * cc + o1);
+                                const double2 t2 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o0);
+                                const double2 t3 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o1);
+                                v[8 * cc + 0] = t0.x; v[8 * cc + 1] = t0.y;
+                                v[8 * cc + 2] = t1.x; v[8 * cc + 3] = t1.y;
+                                v[8 * cc + 4] = t2.x; v[8 * cc + 5] = t2.y;
+                                v[8 * cc + 6] = t3.x; v[8 * cc + 7] = t3.y;
                             }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                a00 = fma(v[2 * j], wv[j].x, a00);
+                                a01 = fma(v[2 * j + 1], wv[j].y, a01);
+                                a10 = fma(v[8 + 2 * j], wv[j].x, a10);
+                                a11 = fma(v[8 + 2 * j + 1], wv[j].y, a11);
+                            }
+                            int ps = pslot + i;
+                            if (ps >= np) ps -= np;
+                            if (ps < SQ) {
+                                const uint32_t t = tq + (uint32_t)(ps * 2 * CS + 2 * 16 * cb);
+                                tmem_st8(t, v);
+                                tmem_st8(t + 16, v + 8);
+                            } else {
+                                double* hp = myhold + (size_t)(ps - SQ) * HSLOT + cb * 16 * 32 + lane;
+#pragma unroll
+                                for (int c = 0; c < 16; ++c) hp[c * 32] = v[c];
+                            }
+                            sp.mark(2);
+                            __syncwarp();       // every lane's reads of the stage are done
+                            if (lane == 0) mbar_arrive(&myempty[st]);
+                            cr.next();
                         }
                         sp.mark(3);
-                        const double colsum = slab_reduce16(acc, lane);
-                        if (lane < 16) pdst[cb * 16 + lane] = colsum;
+                        // columns 2 co, 2 co + 1 summed over the four rq lanes: lanes with rq & 1 == c
+                        // end with column 2 co + c
+                        {
+                            const double s0 = a00 + a01, s1 = a10 + a11;
+                            const bool up = (lane & 1) != 0;
+                            double cs_ = (up ? s1 : s0) + __shfl_xor_sync(0xffffffffu, up ? s0 : s1, 1);
+                            cs_ += __shfl_xor_sync(0xffffffffu, cs_, 2);
+                            if (rq < 2) pdst[cb * 16 + 2 * co + rq] = cs_;
+                        }
                         sp.mark(7);
                     }
                     used += (unsigned)cnt;
@@ -417,6 +449,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         xp.init(kSlabNDX);
         unsigned fin = 0;
         int pslot = 0;
+        const int rq = lane & 3, co = lane >> 2;  // the dot warps' lane layout
         for (int64_t s = 0; s < K * NSPLIT; ++s) {
             const int64_t k = s / NSPLIT;
             const int h = (int)(s - k * NSPLIT);
@@ -430,8 +463,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             const double* dxv = dxring + xp.i * CS;
             if (bh > 0) {
                 for (int i = 0; i < cnt; ++i) {
-                    const int srow = 32 * grp_of(a, k, i) + lane;
-                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                    double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // s8[2 j + t]: row 2 (rq + 4 (j ^ par)) + t
                     int ps = pslot + i;
                     if (ps >= np) ps -= np;
                     if (ps < SQ) {
@@ -441,26 +473,39 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                         for (int c32 = 0; c32 < CS; c32 += 16) {
                             uint32_t uu[32];
 #pragma unroll
-                            for (int s8 = 0; s8 < 2; ++s8) tmem_ld8(t + (uint32_t)(2 * (c32 + 8 * s8)), uu + 16 * s8);
+                            for (int q8 = 0; q8 < 2; ++q8) tmem_ld8(t + (uint32_t)(2 * (c32 + 8 * q8)), uu + 16 * q8);
                             tmem_wait_ld();
+                            const double2 d2 = *reinterpret_cast<const double2*>(dxv + c32 + 2 * co);
 #pragma unroll
-                            for (int c = 0; c < 16; c += 2) {
-                                const double2 d2 = *reinterpret_cast<const double2*>(dxv + c32 + c);
-                                s4[c & 3] = fma(u2d(uu[2 * c], uu[2 * c + 1]), d2.x, s4[c & 3]);
-                                s4[(c + 1) & 3] = fma(u2d(uu[2 * c + 2], uu[2 * c + 3]), d2.y, s4[(c + 1) & 3]);
-                            }
+                            for (int e = 0; e < 8; ++e) s8[e] = fma(u2d(uu[2 * e], uu[2 * e + 1]), d2.x, s8[e]);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) s8[e] = fma(u2d(uu[16 + 2 * e], uu[17 + 2 * e]), d2.y, s8[e]);
                         }
                         tc_fence_before();
                     } else {
                         const double* t = myhold + (size_t)(ps - SQ) * HSLOT + lane;
-#pragma unroll 8
-                        for (int c = 0; c < CS; c += 2) {
-                            const double2 d2 = *reinterpret_cast<const double2*>(dxv + c);
-                            s4[c & 3] = fma(t[c * 32], d2.x, s4[c & 3]);
-                            s4[(c + 1) & 3] = fma(t[(c + 1) * 32], d2.y, s4[(c + 1) & 3]);
+#pragma unroll 1
+                        for (int c32 = 0; c32 < CS; c32 += 16) {
+                            const double2 d2 = *reinterpret_cast<const double2*>(dxv + c32 + 2 * co);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) s8[e] = fma(t[(c32 + e) * 32], d2.x, s8[e]);
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) s8[e] = fma(t[(c32 + 8 + e) * 32], d2.y, s8[e]);
                         }
                     }
-                    const double part = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                    // sum over the eight co lanes (transposing butterfly): lane bit 2 pairs the two
+                    // row-pair orders (my j = 0, 2 are the partner's j = 1, 3), bits 3 and 4 split the
+                    // remaining four rows; the lane ends with the total of row
+                    // 2 (rq + 4 par + 8 b3) + b4
+                    const double q0 = s8[0] + __shfl_xor_sync(0xffffffffu, s8[2], 4);
+                    const double q1 = s8[1] + __shfl_xor_sync(0xffffffffu, s8[3], 4);
+                    const double q2 = s8[4] + __shfl_xor_sync(0xffffffffu, s8[6], 4);
+                    const double q3 = s8[5] + __shfl_xor_sync(0xffffffffu, s8[7], 4);
+                    const bool up3 = (lane & 8) != 0, up4 = (lane & 16) != 0;
+                    const double r0 = (up3 ? q2 : q0) + __shfl_xor_sync(0xffffffffu, up3 ? q0 : q2, 8);
+                    const double r1 = (up3 ? q3 : q1) + __shfl_xor_sync(0xffffffffu, up3 ? q1 : q3, 8);
+                    const double part = (up4 ? r1 : r0) + __shfl_xor_sync(0xffffffffu, up4 ? r0 : r1, 16);
+                    const int srow = 32 * grp_of(a, k, i) + 2 * (rq + 4 * (co & 1) + (up3 ? 8 : 0)) + (up4 ? 1 : 0);
                     if (srow < rows) {
                         if (NSPLIT == 1) rs[srow] += part;
                         else if (h == 0) delta[srow] = part;
