@@ -845,26 +845,35 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
                          sizeof(uint64_t) * (2 * kSlabTMaxStages + 2 * kSlabNP + 3 * kSlabNDX) +
                          sizeof(unsigned long long) * (kSlabAx + kSlabDot) + sizeof(unsigned) * (kSlabDot + 1) + 256;
     const size_t cap = 227 * 1024;
-    // park ring of dot warp d: its groups of (nsplit + X) sub-sequences, X = spare sub-sequences
-    // (a warp may start sub-sequence (k+1, h) once the all-reduce of (k, h - X) freed its slots);
-    // the largest X <= 3 that leaves a load ring of >= 4 stages per warp
-    int xmax = 3, xmin = 0;
-    if (const char* e = dbg_env("ASY_SLABT_EXTRA")) xmax = xmin = std::max(0, atoi(e));
+    // park ring of dot warp d: np slots (TMEM first, then shared-memory hold slots), at least the
+    // nsplit sub-sequences of one block update for each of its groups (deadlock freedom); with
+    // more, the warp may start a sub-sequence while the all-reduces of earlier ones are in flight
     // the last, partial round of groups rotates over the warps (any warp may hold one of them)
     g->rotate = 1;
     if (const char* e = dbg_env("ASY_SLABT_ROTATE")) g->rotate = atoi(e) != 0;
-    // prefer a load ring of >= 8 stages per warp over spare park slots (configs[2]: 3.97 vs
-    // 3.74 TB/s); only then settle for >= 4 stages
+    // Shared memory is split between the load rings (nsw unit stages per dot warp) and the hold
+    // slots that deepen the park rings beyond TMEM.  Both matter: the park ring must cover the
+    // all-reduce chain (~2 block updates of latency), the load ring the HBM latency.  Measured
+    // on configs[2] (np / nsw): 4 / 12 4.27, 5 / 8 4.51, 6 / 4 4.06 TB/s.  Rule: the deepest park
+    // ring (at most 3 spare sub-sequences) that leaves >= 8 stages per warp, else >= 4 stages.
     int nsw = 0, nhold = 0;
     const int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
     const int min_first = ring > 0 ? ring : 8, min_last = ring > 0 ? min_first : 4;
+    int cntmax = 0;
+    for (int d = 0; d < kSlabDot; ++d)
+        cntmax = std::max(cntmax, g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
+                                            : (nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0));
+    int np_hi = (nsplit + 3) * cntmax, np_lo = nsplit * cntmax;  // park slots of the busiest warp
+    if (const char* e = dbg_env("ASY_SLABT_NPARK")) np_hi = np_lo = std::max(np_lo, atoi(e));
     for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 4)
-    for (int X = xmax; X >= xmin; --X) {
+    for (int np = np_hi; np >= np_lo; --np) {
         nhold = 0;
         for (int d = 0; d < kSlabDot; ++d) {
             const int cnt = g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
                                       : (nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0);
-            const int hs = std::max(0, (nsplit + X) * cnt - SQ);
+            // a warp with fewer groups keeps the same depth in block updates
+            const int want = cnt == cntmax ? np : std::max(nsplit * cnt, (np * cnt + cntmax - 1) / cntmax);
+            const int hs = std::max(0, want - SQ);
             g->hoff[d] = nhold;
             g->npark[d] = SQ + hs;
             nhold += hs;

@@ -68,7 +68,10 @@ constexpr int kSlabNDX = kSlabSeq;  // dx ring
 // All-reduce layout: CTA c adds its partial into replica c mod kGaccRep of the slot (148 CTAs
 // adding into one copy serialise ~150 fp64 atomics per address on a few L2 slices); readers
 // sum the replicas.  Arrival counters sit one per 128-byte line (hundreds of warps poll them).
-constexpr int kGaccRep = 8;
+#ifndef ASY_GACC_REP
+#define ASY_GACC_REP 8
+#endif
+constexpr int kGaccRep = ASY_GACC_REP;
 constexpr int kArrivePad = 32;
 constexpr int kSlabMaxStages = 24;
 constexpr int kSlabPad = 32;        // zero doubles after each stage (reads past the last column)

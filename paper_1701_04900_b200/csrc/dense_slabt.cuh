@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                     }
                 }
                 __syncwarp();
+                sp.mark(4);
                 const int64_t need = meta[k & (kSlabNM - 1)].need;
                 if (need > 0) {
                     if (nb > 0)

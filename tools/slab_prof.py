@@ -1,5 +1,5 @@
 """Summarise an ASY_PROF dump of the row-slab kernels: [grid][16 warps][8] clock64 segment sums.
-usage: python tools/slab_prof.py DUMP SEQUENCES [slabt]"""
+usage: python tools/slab_prof.py DUMP SEQUENCES [slabt [SPLIT]]"""
 import sys
 import numpy as np
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 16, 8).astype(np.float64)
@@ -22,3 +22,8 @@ for role, (ws, names) in roles.items():
     if role == "dot":
         per = a[:, ws].sum(axis=2) / K
         print("          per dot warp (cyc/seq, mean over CTAs): " + " ".join(f"{v:8.1f}" for v in per.mean(axis=0)))
+    if len(sys.argv) > 4:  # CTAs [0, SPLIT) own one row group more than the rest
+        sp = int(sys.argv[4])
+        for nm, sl in (("first", slice(0, sp)), ("rest", slice(sp, None))):
+            q = a[sl][:, ws].sum(axis=(0, 1)) / (a[sl].shape[0] * len(ws))
+            print(f"   {nm:>5s} CTAs: " + " ".join(f"{n}={v / K:8.1f}" for n, v in zip(names, q) if n != "-"))
