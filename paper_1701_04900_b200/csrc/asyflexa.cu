@@ -1136,6 +1136,9 @@ static bool use_slab_kernel(const asy_handle* h, const asy_solve_params* sp) {
     return per_sm >= 64.0 * 1024.0;
 }
 
+#ifndef ASY_SPARSE_DELAY_DIV
+#define ASY_SPARSE_DELAY_DIV 4  // auto delay of the CSC kernel: N / this (R25)
+#endif
 #ifndef ASY_SPARSE_LPC
 #define ASY_SPARSE_LPC 2  // lanes per column of the CSC kernel (16 block updates in flight per warp)
 #endif
@@ -1174,6 +1177,7 @@ static int sparse_async_launch(asy_handle* h, const asy_solve_params* sp, int64_
     P.counter = P_<unsigned long long>(h->counter);
     P.ver = P_<unsigned>(h->ver); P.wcnt = P_<unsigned>(h->done); P.lgW = lgW; P.lgS = lgS;
     P.measure_delay = tuning_of(sp).measure_delay != 0;
+    P.use_ver = !(sp->schedule == ASY_SCHED_CYCLIC && delay < h->n);  // D4 implied by D1 (sparse_async.cuh)
     P.dobs = P_<unsigned>(h->dobs);
     h->last_kernel = ASY_KERNEL_SPARSE;
     h->last_delay = (int)delay;
@@ -1227,7 +1231,7 @@ ASY_API int asy_solve(asy_handle* h, const asy_solve_params* sp, asy_solve_stats
     CK(cudaEventRecord(h->ev[2], h->stream));
     if (sp->reset) TRY(reset_state(h, sp->x0, sp->x_mem));
     int64_t delay = sp->max_delay;
-    if (delay < 0) delay = std::max<int64_t>(1, h->nblk / 8);
+    if (delay < 0) delay = std::max<int64_t>(1, h->nblk / (h->kind == ASY_CSC ? ASY_SPARSE_DELAY_DIV : 8));
     delay = std::min<int64_t>(delay, 1 << 22);
     double kernel_ms = 0;
     int64_t launches = sp->reset ? 2 : 0;

@@ -136,8 +136,9 @@ struct Scalars {
 template <int LOSS>
 ASY_HD double loss_prime_t(const Scalars& S, double r, double aux) {
     if (LOSS == LOSS_LS) return S.s2 * r;
-    const double t = -aux * r;  // sigmoid(t)
-    const double sig = t >= 0.0 ? 1.0 / (1.0 + exp(-t)) : exp(t) / (1.0 + exp(t));
+    const double t = -aux * r;  // sigmoid(t) = 1 / (1 + e^-t) (t >= 0), e^t / (1 + e^t) (t < 0): one exp
+    const double e = exp(-fabs(t));
+    const double sig = (t >= 0.0 ? 1.0 : e) / (1.0 + e);
     return -aux * S.minv * sig;
 }
 ASY_HD double loss_prime(const Scalars& S, double r, double aux) {

@@ -305,34 +305,34 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             const int cnt = cnt_of(d, k);  // my row groups in sequence k
             const int ex = extra_of(d, k);
             if (cnt > 0) {
-                // D1 / D4 guards: axpy(k - delay - 1) and axpy(kprev) applied to my rows
-                if (lane == 0) {
+                // D1 / D4 guards: axpy(k - delay - 1) and axpy(kprev) applied to my rows.  Every lane
+                // polls (broadcast shared-memory loads): no lane-0 branch, no warp barrier
+                for (;;) {
                     long long v;
-                    for (;;) {
-                        asm volatile("ld.acquire.cta.shared.b64 %0, [%1];"
-                                     : "=l"(v)
-                                     : "r"(smem_u32(&meta_k[k & (kSlabNM - 1)]))
-                                     : "memory");
-                        if (v == k) break;
-                        __nanosleep(32);
-                    }
+                    asm volatile("ld.acquire.cta.shared.b64 %0, [%1];"
+                                 : "=l"(v)
+                                 : "r"(smem_u32(&meta_k[k & (kSlabNM - 1)]))
+                                 : "memory");
+                    if (v == k) break;
+                    __nanosleep(32);
                 }
-                __syncwarp();
                 sp.mark(4);
                 const int64_t need = meta[k & (kSlabNM - 1)].need;
-                if (need > 0) {
-                    if (nb > 0)
-                        while (ld_acquire_cta_u64(&progress[d]) < (unsigned long long)need) __nanosleep(20);
-                    if (ex >= 0)
-                        while (ld_acquire_cta_u64(&xprog[ex]) < (unsigned long long)need) __nanosleep(20);
-                }
                 // observed delay: the rows about to be read lack exactly sequences progress..k-1
-                if (lane == 0) {
-                    unsigned long long have = nb > 0 ? ld_acquire_cta_u64(&progress[d]) : (unsigned long long)k;
+                unsigned long long have = nb > 0 ? ld_acquire_cta_u64(&progress[d]) : (unsigned long long)k;
+                if (ex >= 0) {
+                    const unsigned long long hx = ld_acquire_cta_u64(&xprog[ex]);
+                    if (hx < have) have = hx;
+                }
+                while ((long long)have < need) {
+                    __nanosleep(20);
+                    have = nb > 0 ? ld_acquire_cta_u64(&progress[d]) : (unsigned long long)k;
                     if (ex >= 0) {
                         const unsigned long long hx = ld_acquire_cta_u64(&xprog[ex]);
                         if (hx < have) have = hx;
                     }
+                }
+                {
                     const long long miss = k - (long long)have;
                     if (miss > dmax_local) dmax_local = miss;
                 }

@@ -25,7 +25,9 @@
 //     so those windows end strictly before batch t, and S > (delta + 2) / W + 2, so a slot
 //     is reused only after its previous window is complete;
 //   * own-block freshness D4 [PAPER.md:233]: ver[j] = number of applied updates of block j;
-//     the update of epoch e waits for ver[j] >= e.
+//     the update of epoch e waits for ver[j] >= e.  With the cyclic schedule and delta < N the
+//     block's previous update (sequence k - N) is among the sequences D1 already waits for, so
+//     ver[] is neither read nor written (use_ver = 0: two L2 operations per update less).
 // delta == 0 gives BS = W = 1 and the sequential (d^k = 0) scheme, bit-reproducible.
 // Observed delay: sampled on every 32nd batch of a warp, after a refresh of its window count wm:
 // the largest k - k_first(W * wm) over the batch's sequences at read time (an upper bound on d^k
@@ -59,6 +61,7 @@ struct SparseAsyncParams {
     int lgS;                      // S = 2^lgS window slots
     unsigned* dobs;               // observed delay (max)
     int measure_delay;            // sample the observed delay (asy_tuning.measure_delay)
+    int use_ver;                  // 0: D4 is implied by D1 (cyclic schedule, delay < N): ver[] is not touched
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32_g(const unsigned* p) {
@@ -128,13 +131,19 @@ __global__ void sparse_async_init(SparseAsyncParams P) {
 #ifndef ASY_SPARSE_CLAIM
 #define ASY_SPARSE_CLAIM 1  // batches claimed per atomic
 #endif
+#ifndef ASY_SPARSE_MINB
+#define ASY_SPARSE_MINB 5  // resident CTAs per SM the register allocation must allow (5: <= 102 registers, 20 warps)
+#endif
+#ifndef ASY_SPARSE_RELOAD
+#define ASY_SPARSE_RELOAD 0
+#endif
 constexpr int kSparseThreads = ASY_SPARSE_THREADS;
 constexpr int kSparseClaim = ASY_SPARSE_CLAIM;
 constexpr int kSparseCh = ASY_SPARSE_CH;
 
 // LPC lanes per column (1, 2, 4 or 8): batch lanes b = lane / LPC, element lane e = lane % LPC.
 template <int LOSS, int LPC>
-__global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyncParams P) {
+__global__ void __launch_bounds__(kSparseThreads, ASY_SPARSE_MINB) sparse_async_kernel(SparseAsyncParams P) {
     const int lane = threadIdx.x & 31;
     const int bl = lane / LPC, el = lane % LPC;
     const unsigned cmask = LPC == 32 ? 0xffffffffu : (((1u << LPC) - 1u) << (bl * LPC));
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
             h.s = __ldg(&P.colptr[h.j]);
             h.s1 = __ldg(&P.colptr[h.j + 1]);
             if (el == 0) {
-                h.vj = ld_acquire_u32_g(&P.ver[h.j]);
+                if (P.use_ver) h.vj = ld_acquire_u32_g(&P.ver[h.j]);
                 h.tj = __ldg(&P.tau[h.j]);
             }
         }
@@ -202,7 +211,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
         if (pend < 0) return;
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         __syncwarp();
-        if (pend_live && el == 0) red_relaxed_u32_g(&P.ver[pend_j], 1u);
+        if (P.use_ver && pend_live && el == 0) red_relaxed_u32_g(&P.ver[pend_j], 1u);
         if (lane == 0) red_relaxed_u32_g(&P.wcnt[(pend >> lgW) & Smask], 1u);
         pend = -1;
     };
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
         const long long kd = cur.e * N + i0 + nlive - 1 - P.delay - 1;
         const long long nw = kd >= 0 ? (batch_of(kd) + (1ll << lgW)) >> lgW : 0;  // windows needed
         // D4: the previous update of this block applied
-        const bool d4 = cur.live && el == 0 && cur.vj < (unsigned)cur.e;
+        const bool d4 = P.use_ver && cur.live && el == 0 && cur.vj < (unsigned)cur.e;
         const bool d4any = __any_sync(0xffffffffu, d4);
         if (wmw < nw || d4any) release();
         // every 32nd batch of a warp refreshes its window count even when the guard holds (the
@@ -323,7 +332,14 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_async_kernel(SparseAsyn
 #pragma unroll
                 for (int u = 0; u < kSparseCh; ++u) {
                     const int64_t q = el + (int64_t)u * LPC;
+#if ASY_SPARSE_RELOAD
+                    // (values and rows re-read at scatter time -- L1 / L2 hits -- instead of held in
+                    // registers across the gathers: 24 registers less, one more resident CTA per SM)
+                    if (q < cnt)
+                        red_relaxed_add_f64_g(&P.r[2 * (int64_t)__ldg(&P.rowidx[cur.s + q])], __ldg(&P.vals[cur.s + q]) * d);
+#else
                     if (q < cnt) red_relaxed_add_f64_g(&P.r[2 * (int64_t)rows[u]], vv[u] * d);
+#endif
                 }
                 for (int64_t q = el + (int64_t)kSparseCh * LPC; q < cnt; q += LPC)
                     red_relaxed_add_f64_g(&P.r[2 * (int64_t)__ldg(&P.rowidx[cur.s + q])], __ldg(&P.vals[cur.s + q]) * d);

@@ -36,7 +36,8 @@ for rep in range(reps):
     for n in names:
         A, S = mods[n], solvers[n]
         sc = A.ASY_SCHED_CYCLIC if sched == "cyclic" else A.ASY_SCHED_RANDOM
-        st = S.solve(sweeps=sw, reset=True, schedule=sc, seed=rep)
+        st = S.solve(sweeps=sw, reset=True, schedule=sc, seed=rep, workers=int(os.environ.get("WORKERS", "0")),
+                     max_delay=int(os.environ.get("MAX_DELAY", "-1")))
         if P.kind == "dense":
             rate = f"{8.0 * P.m * P.n * sw / (st.kernel_ms * 1e-3) / 1e9:8.1f} GB/s"
         else:
