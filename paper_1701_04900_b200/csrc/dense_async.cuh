@@ -346,6 +346,22 @@ __device__ __forceinline__ double transpose_reduce8(double (&v)[8], int lane) {
     return t + __shfl_xor_sync(0xffffffffu, t, 16);
 }
 
+// 16 doubles of a 32 x 16 sub-tile for one lane (see the dot warps): two columns (stride ld),
+// four row pairs at offsets o0, o1, 16 + o0, 16 + o1 from a.
+__device__ __forceinline__ void load_subtile(const double* a, int ld, int o0, int o1, double (&v)[16]) {
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        const double2 t0 = *reinterpret_cast<const double2*>(a + cc * ld + o0);
+        const double2 t1 = *reinterpret_cast<const double2*>(a + cc * ld + o1);
+        const double2 t2 = *reinterpret_cast<const double2*>(a + cc * ld + 16 + o0);
+        const double2 t3 = *reinterpret_cast<const double2*>(a + cc * ld + 16 + o1);
+        v[8 * cc + 0] = t0.x; v[8 * cc + 1] = t0.y;
+        v[8 * cc + 2] = t1.x; v[8 * cc + 3] = t1.y;
+        v[8 * cc + 4] = t2.x; v[8 * cc + 5] = t2.y;
+        v[8 * cc + 6] = t3.x; v[8 * cc + 7] = t3.y;
+    }
+}
+
 // BT = block width padded to a power of two >= 8 (panel columns, TMEM row layout);
 // RPL = panel rows per lane (R = 32*RPL); NS = smem stages (kPairs or 2*kPairs:
 // a second stage per pair overlaps the next panel's load with this one's dot).
@@ -603,6 +619,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         const uint32_t tlane = tmem_base + ((uint32_t)(32 * q) << 16);
         static_assert(kSlotsPerAx * kAxpyPerPair == kTmemSlots, "axpy warp h owns TMEM slots h*kSlotsPerAx..");
         unsigned tm_used0 = 0u, tm_used1 = 0u;  // panels parked for the pair's axpy warp h = 0 / 1
+        const int rq = lane & 3, co = lane >> 2;
+        const int o0 = 8 * (co & 1), o1 = 8 - o0;  // row-pair offsets of j = 0, 1 (j = 2, 3: + 16)
         SegProf sp;
         sp.start();
         for (long long j = 0;; ++j) {
@@ -652,6 +670,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const int i = lane + 32 * qq;
                 rsm[i] = (r0 + i) < P.m ? loss_prime_t<LOSS>(P.S, rsm[i], rsm[R + i]) : 0.0;
             }
+            __syncwarp();  // (the dot pass reads w of other lanes' rows)
             sp.mark(1);
             // a free TMEM slot now?  then dot and park in ONE pass over shared memory
             int parked = 0;
@@ -663,6 +682,53 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             }
             const int tslot_idx = h * kSlotsPerAx + (int)(tm_used % kSlotsPerAx);
             const uint32_t tslot = tlane + (uint32_t)(tslot_idx * kSlotCols);
+            if constexpr (BT >= 16) {
+            // Lane layout of a 32 x 16 sub-tile (rows 32 qq.., columns g0..): lane (co = lane >> 2,
+            // rq = lane & 3) owns columns g0 + 2 co, + 1 and the row pairs rq + 4 (j ^ (co & 1)),
+            // j < 4, read as double2 (8 conflict-free 16-byte loads per sub-tile).  The sum over
+            // rows is in-lane over all RPL sub-tiles and takes two shuffles per 16 columns (a
+            // lane-per-row layout needs a 16-shuffle butterfly); the axpy warps, two per dot warp,
+            // pay a 7-shuffle transposing sum per 32 rows instead.
+#pragma unroll
+            for (int g0 = 0; g0 < BT; g0 += GW) {
+                double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+#pragma unroll kRoll
+                for (int qq = 0; qq < RPL; ++qq) {
+                    double v[16];  // v[8 cc + 2 j + t] = A[row 32 qq + 2 (rq + 4 (j ^ par)) + t][column g0 + 2 co + cc]
+                    load_subtile(pan + (size_t)(g0 + 2 * co) * R + 32 * qq + 2 * rq, R, o0, o1, v);
+                    const double* wp = rsm + 32 * qq + 2 * rq;
+                    const double2 w0 = *reinterpret_cast<const double2*>(wp + o0);
+                    const double2 w1 = *reinterpret_cast<const double2*>(wp + o1);
+                    const double2 w2 = *reinterpret_cast<const double2*>(wp + 16 + o0);
+                    const double2 w3 = *reinterpret_cast<const double2*>(wp + 16 + o1);
+                    a00 = fma(v[0], w0.x, a00); a01 = fma(v[1], w0.y, a01);
+                    a10 = fma(v[8], w0.x, a10); a11 = fma(v[9], w0.y, a11);
+                    a00 = fma(v[2], w1.x, a00); a01 = fma(v[3], w1.y, a01);
+                    a10 = fma(v[10], w1.x, a10); a11 = fma(v[11], w1.y, a11);
+                    a00 = fma(v[4], w2.x, a00); a01 = fma(v[5], w2.y, a01);
+                    a10 = fma(v[12], w2.x, a10); a11 = fma(v[13], w2.y, a11);
+                    a00 = fma(v[6], w3.x, a00); a01 = fma(v[7], w3.y, a01);
+                    a10 = fma(v[14], w3.x, a10); a11 = fma(v[15], w3.y, a11);
+                    if (parked) {
+                        const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
+                        tmem_st8(trow, v);
+                        tmem_st8(trow + 16, v + 8);
+                    }
+                }
+                // columns g0 + 2 co, + 1 summed over the four rq lanes: lanes with rq & 1 == c end
+                // with column g0 + 2 co + c
+                const double s0 = a00 + a01, s1 = a10 + a11;
+                const bool up = (lane & 1) != 0;
+                double colsum = (up ? s1 : s0) + __shfl_xor_sync(0xffffffffu, up ? s0 : s1, 1);
+                colsum += __shfl_xor_sync(0xffffffffu, colsum, 2);
+                const int cidx = g0 + 2 * co + rq;
+                if (rq < 2 && cidx < nc) {
+                    if (P.deterministic) P.part[p * Bmax + cidx] = colsum;
+                    else atomicAdd(&gacc[cidx], colsum);
+                }
+            }
+            } else {
+                // (blocks of <= 8 columns: lane = row, 8-column butterfly)
 #pragma unroll
             for (int g0 = 0; g0 < BT; g0 += GW) {
                 double acc[GW];
@@ -691,6 +757,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                     else atomicAdd(&gacc[g0 + lane], colsum);
                 }
             }
+            }
             ASY_TRACE(P, md.t, 3);
             sp.mark(2);
             if (!parked && P.use_tmem) {
@@ -710,6 +777,19 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 sp.mark(3);
                 if (parked) {
                     tc_fence_after();
+                    if constexpr (BT >= 16) {
+#pragma unroll
+                    for (int g0 = 0; g0 < BT; g0 += GW) {
+#pragma unroll kRoll
+                        for (int qq = 0; qq < RPL; ++qq) {
+                            double v[16];
+                            load_subtile(pan + (size_t)(g0 + 2 * co) * R + 32 * qq + 2 * rq, R, o0, o1, v);
+                            const uint32_t trow = tslot + (uint32_t)(qq * cols_per_row + 2 * g0);
+                            tmem_st8(trow, v);
+                            tmem_st8(trow + 16, v + 8);
+                        }
+                    }
+                    } else {
 #pragma unroll
                     for (int g0 = 0; g0 < BT; g0 += GW) {
 #pragma unroll kRoll
@@ -722,6 +802,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #pragma unroll
                             for (int s8 = 0; s8 < GW / 8; ++s8) tmem_st8(trow + 16 * s8, v + 8 * s8);
                         }
+                    }
                     }
                 }
             }
@@ -756,6 +837,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
         uint64_t* myfull = rfull + ax * kRing;
         uint64_t* myempty = rempty + ax * kRing;
         unsigned tm_fin = 0;
+        const int rq = lane & 3, co = lane >> 2;  // the dot warps' lane layout
         long long pend_slot = -1, pend_b = -1, pend_k = 0;  // completion of the previous panel, issued late
         auto complete = [&]() {
             if (pend_slot >= 0 && lane == 0) {
@@ -871,6 +953,70 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
             const long long r0 = p * R;
             if (hd.parked) tc_fence_after();
             if (nz) {
+                if constexpr (BT >= 16) {
+#pragma unroll kRoll
+                for (int qq = 0; qq < RPL; ++qq) {
+                    long long row;
+                    double dsum;
+                    if (hd.parked) {
+                        // the dot warp's lane layout: s8[2 j + t] = this lane's two columns' share of
+                        // row 32 qq + 2 (rq + 4 (j ^ par)) + t
+                        double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                        const uint32_t trow = tquarter + (uint32_t)((hd.parked - 1) * kSlotCols + qq * cols_per_row);
+#pragma unroll
+                        for (int c32 = 0; c32 < BT; c32 += 32) {
+                            constexpr int n8max = BT < 32 ? BT / 8 : 4;
+                            uint32_t uu[16 * n8max];
+#pragma unroll
+                            for (int q8 = 0; q8 < n8max; ++q8) tmem_ld8(trow + 2 * (c32 + 8 * q8), uu + 16 * q8);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int sub = 0; sub < n8max / 2; ++sub) {
+                                const double2 d2 = *reinterpret_cast<const double2*>(dv + c32 + 16 * sub + 2 * co);
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    s8[e] = fma(u2d(uu[32 * sub + 2 * e], uu[32 * sub + 2 * e + 1]), d2.x, s8[e]);
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    s8[e] = fma(u2d(uu[32 * sub + 16 + 2 * e], uu[32 * sub + 17 + 2 * e]), d2.y, s8[e]);
+                            }
+                        }
+                        // sum over the eight co lanes (transposing butterfly): lane bit 2 pairs the two
+                        // row-pair orders (my j = 0, 2 are the partner's j = 1, 3), bits 3 and 4 split
+                        // the remaining four rows
+                        const double q0 = s8[0] + __shfl_xor_sync(0xffffffffu, s8[2], 4);
+                        const double q1 = s8[1] + __shfl_xor_sync(0xffffffffu, s8[3], 4);
+                        const double q2 = s8[4] + __shfl_xor_sync(0xffffffffu, s8[6], 4);
+                        const double q3 = s8[5] + __shfl_xor_sync(0xffffffffu, s8[7], 4);
+                        const bool up3 = (lane & 8) != 0, up4 = (lane & 16) != 0;
+                        const double r0s = (up3 ? q2 : q0) + __shfl_xor_sync(0xffffffffu, up3 ? q0 : q2, 8);
+                        const double r1s = (up3 ? q3 : q1) + __shfl_xor_sync(0xffffffffu, up3 ? q1 : q3, 8);
+                        dsum = (up4 ? r1s : r0s) + __shfl_xor_sync(0xffffffffu, up4 ? r0s : r1s, 16);
+                        row = r0 + 32 * qq + 2 * (rq + 4 * (co & 1) + (up3 ? 8 : 0)) + (up4 ? 1 : 0);
+                    } else {
+                        double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+                        row = r0 + lane + 32 * qq;
+                        if (row < P.m) {
+                            // re-read the panel row from global memory (L2, usually)
+                            const double* a = P.A + c0 * P.lda + row;
+#pragma unroll 1
+                            for (int c8 = 0; c8 < nc; c8 += 8) {
+                                double av[8];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) av[i] = (c8 + i) < nc ? __ldg(a + (c8 + i) * P.lda) : 0.0;
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) acc4[i & 3] = fma(av[i], dv[c8 + i], acc4[i & 3]);
+                            }
+                        }
+                        dsum = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+                    }
+#ifdef ASY_DIAG_NO_RED
+                    if (row < P.m && dsum == 12345.0) P.r[row] = dsum;
+#else
+                    if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
+#endif
+                }
+                } else {
 #pragma unroll kRoll
                 for (int qq = 0; qq < RPL; ++qq) {
                     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -909,6 +1055,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 #else
                     if (row < P.m && dsum != 0.0) atomicAdd(&P.r[row], dsum);
 #endif
+                }
                 }
             }
             ASY_TRACE(P, md.t, 9);
