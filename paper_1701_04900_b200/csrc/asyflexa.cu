@@ -857,7 +857,8 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // on configs[2] (np / nsw): 4 / 12 4.27, 5 / 8 4.51, 6 / 4 4.06 TB/s.  Rule: the deepest park
     // ring (at most 3 spare sub-sequences) that leaves >= 8 stages per warp, else >= 4 stages.
     int nsw = 0, nhold = 0;
-    const int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
+    int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
+    if (const char* e = dbg_env("ASY_SLABT_RING")) ring = atoi(e);
     const int min_first = ring > 0 ? ring : 8, min_last = ring > 0 ? min_first : 4;
     int cntmax = 0;
     for (int d = 0; d < kSlabDot; ++d)
