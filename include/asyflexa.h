@@ -143,7 +143,7 @@ typedef struct {
     double gamma;          /* fixed stepsize, 0 < gamma <= 1  [PAPER.md:154] */
     int64_t sweeps;        /* passes: async = sweeps*N block updates; Jacobi = sweeps iterations */
     int64_t max_delay;     /* async: max block updates in flight besides the one being read
-                              (Assumption D1's delta [PAPER.md:224]); -1 = auto (N/8), 0 = sequential */
+                              (Assumption D1's delta [PAPER.md:224]); -1 = auto (N/8; N/4 for CSC problems), 0 = sequential */
     int32_t reset;         /* 1: start from x0 (NULL: zeros), residual recomputed; 0: continue */
     int32_t x_mem;         /* memory kind of x0 / x_out */
     const double* x0;      /* n entries or NULL */
