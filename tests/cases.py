@@ -62,6 +62,9 @@ def _make_case(name):
     if name == "block100":        # blocks of 100: padded to 128, last sub-sequence 4 columns wide
         return inputs.dense_lasso(210, 470, nnz_frac=0.02, sigma=0.01, lam_frac=0.05, block=100,
                                   gamma=0.9, seed=13)
+    if name == "block12":         # blocks of 12: padded to 16 columns (one ragged 16-column group), last block 8 wide
+        return inputs.dense_lasso(230, 500, nnz_frac=0.02, sigma=0.01, lam_frac=0.05, block=12,
+                                  gamma=0.9, seed=15)
     if name == "sparse_logistic":  # config 4 recipe, small
         P = inputs.sparse_logistic(300, 900, density=0.03, seed=6, lam_frac=0.02)
         s, e = P.colptr[100], P.colptr[101]          # make column 100 empty (edge case)

@@ -39,7 +39,7 @@ def _rel_f(a, b):
 
 
 SEQ_CASES = ["config0", "dense_ragged", "nonconvex", "large_block", "sparse_logistic", "sparse_ls",
-             "dense_logistic", "dc_exp", "dc_log"]
+             "dense_logistic", "dc_exp", "dc_log", "block12"]
 
 
 # ----------------------------------------------------------------------------- schedule
@@ -185,7 +185,7 @@ def test_stationarity_matches_oracle(A, case):
 
 # ----------------------------------------------------------------------------- asynchronous
 ASYNC_CASES = ["config0", "dense_ragged", "dense_normalized", "nonconvex", "large_block",
-               "sparse_logistic", "sparse_ls", "dense_logistic", "dc_exp", "dc_log"]
+               "sparse_logistic", "sparse_ls", "dense_logistic", "dc_exp", "dc_log", "block12"]
 
 
 def _residual_drift(A, S, P):
@@ -255,7 +255,7 @@ DENSE_VARIANTS = {
 
 
 @pytest.mark.parametrize("variant", sorted(DENSE_VARIANTS))
-@pytest.mark.parametrize("case", ["dense_ragged", "large_block", "nonconvex"])
+@pytest.mark.parametrize("case", ["dense_ragged", "large_block", "nonconvex", "block12"])
 def test_dense_kernel_variants(A, case, variant):
     """Every geometry / code path of the dense asynchronous kernels: sequential parity
     (per iteration) and asynchronous convergence to the oracle's solution."""
