@@ -854,26 +854,29 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // Shared memory is split between the load rings (nsw unit stages per dot warp) and the hold
     // slots that deepen the park rings beyond TMEM.  Both matter: the park ring must cover the
     // all-reduce chain (~2 block updates of latency), the load ring the HBM latency.  Measured
-    // on configs[2] (np / nsw): 4 / 12 4.27, 5 / 8 4.51, 6 / 4 4.06 TB/s.  Rule: the deepest park
-    // ring (at most 3 spare sub-sequences) that leaves >= 8 stages per warp, else >= 4 stages.
+    // on configs[2] (np / nsw): 4 / 12 4.27, 5 / 8 4.51, 5 / 6 4.56, 6 / 4 4.06 TB/s; on configs[3]:
+    // 8 / 12 4.2, 9 / 10 4.93, 10 / 8 5.04, 11 / 6 5.14, 12 / 4 5.03.  Rule: the deepest park ring
+    // (at most 3 spare sub-sequences) that leaves >= 6 stages per warp, else >= 4 stages.
     int nsw = 0, nhold = 0;
     int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
     if (const char* e = dbg_env("ASY_SLABT_RING")) ring = atoi(e);
-    const int min_first = ring > 0 ? ring : 8, min_last = ring > 0 ? min_first : 4;
+    const int min_first = ring > 0 ? ring : 6, min_last = ring > 0 ? min_first : 4;
     int cntmax = 0;
     for (int d = 0; d < kSlabDot; ++d)
         cntmax = std::max(cntmax, g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
                                             : (nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0));
-    int np_hi = (nsplit + 3) * cntmax, np_lo = nsplit * cntmax;  // park slots of the busiest warp
+    // (deadlock freedom needs only one sub-sequence's slots, np >= cntmax: sub-sequence (k, h) then
+    // waits for the axpy of (k, h - 1), whose all-reduce needs no CTA to go beyond (k, h - 1))
+    int np_hi = (nsplit + 3) * cntmax, np_lo = cntmax;  // park slots of the busiest warp
     if (const char* e = dbg_env("ASY_SLABT_NPARK")) np_hi = np_lo = std::max(np_lo, atoi(e));
-    for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 4)
+    for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 2)
     for (int np = np_hi; np >= np_lo; --np) {
         nhold = 0;
         for (int d = 0; d < kSlabDot; ++d) {
             const int cnt = g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
                                       : (nrg > d ? (nrg - d + kSlabDot - 1) / kSlabDot : 0);
             // a warp with fewer groups keeps the same depth in block updates
-            const int want = cnt == cntmax ? np : std::max(nsplit * cnt, (np * cnt + cntmax - 1) / cntmax);
+            const int want = cnt == cntmax ? np : std::max(cnt, (np * cnt + cntmax - 1) / cntmax);
             const int hs = std::max(0, want - SQ);
             g->hoff[d] = nhold;
             g->npark[d] = SQ + hs;
@@ -882,6 +885,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
         nsw = kSlabTMaxStages / kSlabDot;
         if (ring > 0) nsw = std::max(1, std::min(nsw, ring));
         while (nsw > min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
+        if (ring <= 0 && nsw > min_nsw && (nsw & 1)) --nsw;  // (an odd ring halves the issuing lanes: -25%)
         if (nsw >= min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
         nsw = 0;
     }
