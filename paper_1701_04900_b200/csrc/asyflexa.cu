@@ -838,7 +838,8 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     const int nrg = (int)((ngt + grid0 - 1) / grid0);  // most groups of a CTA
     const int64_t Rs = 32 * (int64_t)nrg;
     if ((nrg + kSlabDot - 1) / kSlabDot > kSlabTMaxG) return false;
-    const size_t unit = sizeof(double) * 32 * 16, hslot = sizeof(double) * 32 * CS;
+    const int UC = std::min(kSlabTUnitCols, CS);  // unit columns (dense_slabt.cuh)
+    const size_t unit = sizeof(double) * 32 * UC, hslot = sizeof(double) * 32 * CS;
     const int64_t RsP = (Rs + 1) & ~1ll;
     const size_t fixed = sizeof(double) * (3 * RsP + kSlabDot * kSlabTMaxG * 32 + (size_t)(kSlabNP * kSlabDot + kSlabNDX) * CS) +
                          (sizeof(SeqMeta) + sizeof(long long)) * kSlabNM +
@@ -860,7 +861,8 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     int nsw = 0, nhold = 0;
     int ring = tuning_of(sp).slab_ring;  // (test / measurement override of the ring depth)
     if (const char* e = dbg_env("ASY_SLABT_RING")) ring = atoi(e);
-    const int min_first = ring > 0 ? ring : 6, min_last = ring > 0 ? min_first : 4;
+    const int per4k = UC / 16;  // 4 KB per unit stage
+    const int min_first = ring > 0 ? ring : std::max(2, 6 / per4k), min_last = ring > 0 ? min_first : std::max(1, 4 / per4k);
     int cntmax = 0;
     for (int d = 0; d < kSlabDot; ++d)
         cntmax = std::max(cntmax, g->rotate ? nrg / kSlabDot + (nrg % kSlabDot ? 1 : 0)
@@ -869,7 +871,7 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
     // waits for the axpy of (k, h - 1), whose all-reduce needs no CTA to go beyond (k, h - 1))
     int np_hi = (nsplit + 3) * cntmax, np_lo = cntmax;  // park slots of the busiest warp
     if (const char* e = dbg_env("ASY_SLABT_NPARK")) np_hi = np_lo = std::max(np_lo, atoi(e));
-    for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= 2)
+    for (int min_nsw = min_first; min_nsw >= min_last && nsw == 0; min_nsw -= std::max(1, 2 / per4k))
     for (int np = np_hi; np >= np_lo; --np) {
         nhold = 0;
         for (int d = 0; d < kSlabDot; ++d) {
@@ -885,7 +887,8 @@ static bool slabt_geometry(const asy_handle* h, const asy_solve_params* sp, Slab
         nsw = kSlabTMaxStages / kSlabDot;
         if (ring > 0) nsw = std::max(1, std::min(nsw, ring));
         while (nsw > min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit > cap) --nsw;
-        if (ring <= 0 && nsw > min_nsw && (nsw & 1)) --nsw;  // (an odd ring halves the issuing lanes: -25%)
+        // (an odd ring of 4 KB units halves the issuing lanes: -25%; 8 KB boxes need only one lane per ring)
+        if (per4k == 1 && ring <= 0 && nsw > min_nsw && (nsw & 1)) --nsw;
         if (nsw >= min_nsw && fixed + nhold * hslot + kSlabDot * nsw * unit <= cap) break;
         nsw = 0;
     }
@@ -915,7 +918,8 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return h->fail(ASY_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     CUtensorMap tmap;
-    const int W = B < 16 ? (int)B : 16;  // unit box: 32 rows x 16 columns
+    const int UCk = std::min(kSlabTUnitCols, geo.cs);
+    const int W = B < UCk ? (int)B : UCk;  // unit box: 32 rows x UC columns
     cuuint64_t dims[2] = {(cuuint64_t)h->m, (cuuint64_t)h->n};
     cuuint64_t strides[1] = {(cuuint64_t)(h->lda * sizeof(double))};
     cuuint32_t box[2] = {32u, (cuuint32_t)W};
@@ -932,7 +936,7 @@ static int dense_slabt_launch(asy_handle* h, const asy_solve_params* sp, const S
     SlabParams P{};
     P.m = h->m; P.n = h->n; P.B = B; P.nblk = h->nblk;
     P.Rs = geo.Rs; P.Rc = 32; P.nch = (int)((geo.Rs + 31) / 32); P.hold = 1;
-    P.nst = kSlabDot * geo.nsw; P.nsa = geo.nhold; P.stage_dbl = 32 * 16;
+    P.nst = kSlabDot * geo.nsw; P.nsa = geo.nhold; P.stage_dbl = 32 * UCk;
     P.r = P_<double>(h->r); P.aux = P_<double>(h->b); P.tau = P_<double>(h->tau);
     P.x0 = P_<double>(h->x); P.x1 = P_<double>(h->xalt);
     P.S = h->S; P.gamma = sp->gamma; P.sched = sp->schedule; P.seed = sp->seed; P.epoch0 = h->epochs;

@@ -45,6 +45,11 @@
 namespace asy {
 
 constexpr int kSlabTMaxStages = 64;  // 4 dot warps x nsw
+#ifndef ASY_SLABT_UC
+#define ASY_SLABT_UC 32
+#endif
+constexpr int kSlabTUnitCols = ASY_SLABT_UC;  // columns per unit stage: a 32 x 32 box halves the per-unit
+                                              // mbarrier / issue overhead of 32 x 16 boxes
 constexpr int kSlabTMaxG = 4;        // row groups per warp per sequence (slabs <= 512 rows)
 
 template <int BMAX, int LOSS, int CS_ = 32>
@@ -53,7 +58,9 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
     constexpr int CS = CS_;                    // columns of a sub-sequence (32, or 64 for blocks of 33-64)
     constexpr int NSPLIT = BMAX / CS;          // sub-sequences (all-reduces) per block update
     constexpr int SQ = 256 / CS;               // TMEM park slots per lane quarter (2*CS b32 columns)
-    constexpr int UNIT = 32 * 16;              // doubles per unit stage (4 KB)
+    constexpr int UC = kSlabTUnitCols < CS ? kSlabTUnitCols : CS;  // columns of a unit (one TMA box / mbarrier)
+    constexpr int NH = UC / 16;                // 16-column halves of a unit
+    constexpr int UNIT = 32 * UC;              // doubles per unit stage (4 or 8 KB)
     constexpr int HSLOT = 32 * CS;             // doubles per smem hold slot
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int nsw = P.nst / kSlabDot;
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         // and issue in the same instruction whenever their ring has a free stage (a thread
         // sustains only ~1 bulk copy per ~450 ns, tools/mb_tma.cu), and no ring waits for
         // another (a dot warp waiting for a park slot holds only its own stages).
-        const int W = B < 16 ? B : 16;  // unit columns loaded
+        const int W = B < UC ? B : UC;  // unit columns loaded
         const uint32_t box_bytes = 32u * (uint32_t)W * 8u;
         const uint64_t pol = policy_evict_first();
         // lanes (d, e), d = lane & 3, e = lane >> 2 < NL: ring d's units u = e (mod NL) go to
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             if (++ii == cnt) {
                 ii = 0;
                 const int bh = min(CS, B - ih * CS);
-                if (++icb == (bh <= 0 ? 0 : (bh + 15) >> 4)) {
+                if (++icb == (bh <= 0 ? 0 : (bh + UC - 1) / UC)) {
                     icb = 0;
                     if (++ih == NSPLIT) {
                         ih = 0;
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
             if (ok) {
                 const int g = grp_of(d, ik, ii);
                 mbar_arrive_expect_tx(&dfull[st], box_bytes);
-                slab_tma_2d(dstage + (size_t)st * UNIT, &tmap, (int)(row0 + 32 * g), (int)(icol0 + ih * CS + icb * 16),
+                slab_tma_2d(dstage + (size_t)st * UNIT, &tmap, (int)(row0 + 32 * g), (int)(icol0 + ih * CS + icb * UC),
                             &dfull[st], pol);
                 ist += NL;
                 if (ist >= nsw) { ist -= nsw; iph ^= 1u; first = 0; }
@@ -282,9 +289,9 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
         uint64_t* myempty = dempty + d * nsw;
         const double* mystage = dstage + (size_t)d * nsw * UNIT;
         // column blocks of sub-sequence h (blocks narrower than BMAX skip the empty ones)
-        auto ncb_of = [&](int h) {
+        auto ncb_of = [&](int h) {  // units of sub-sequence h
             const int bh = min(CS, B - h * CS);
-            return bh <= 0 ? 0 : (bh + 15) >> 4;
+            return bh <= 0 ? 0 : (bh + UC - 1) / UC;
         };
         RingPos pp;
         pp.init(kSlabNP);
@@ -360,51 +367,60 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                     }
                     tc_fence_after();
                     sp.mark(5);
+                    const int bhh = min(CS, B - h * CS);  // columns of this sub-sequence
 #pragma unroll 1
                     for (int cb = 0; cb < ncb; ++cb) {
-                        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;  // columns 2 co (x, y rows), 2 co + 1
+                        // acc[hf][0..3]: columns 2 co (x, y rows), 2 co + 1 of 16-column half hf of the unit
+                        double acc[NH][4];
+#pragma unroll
+                        for (int hf = 0; hf < NH; ++hf) acc[hf][0] = acc[hf][1] = acc[hf][2] = acc[hf][3] = 0.0;
 #pragma unroll 1
                         for (int i = 0; i < cnt; ++i) {
                             const int st = cr.i;
                             sp.mark(3);
                             mbar_wait(&myfull[st], cr.ph);
                             sp.mark(6);
-                            const double* a = mystage + (size_t)st * UNIT + lbase;
                             const double* wp = mywscr + i * 32 + 2 * rq;
                             double2 wv[4];
                             wv[0] = *reinterpret_cast<const double2*>(wp + o0);
                             wv[1] = *reinterpret_cast<const double2*>(wp + o1);
                             wv[2] = *reinterpret_cast<const double2*>(wp + 16 + o0);
                             wv[3] = *reinterpret_cast<const double2*>(wp + 16 + o1);
-                            double v[16];  // v[8 cc + 2 j + t] = A[row 2 (rq + 4 (j ^ par)) + t][column 2 co + cc]
-#pragma unroll
-                            for (int cc = 0; cc < 2; ++cc) {
-                                const double2 t0 = *reinterpret_cast<const double2*>(a + 32 * cc + o0);
-                                const double2 t1 = *reinterpret_cast<const double2*>(a + 32 * cc + o1);
-                                const double2 t2 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o0);
-                                const double2 t3 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o1);
-                                v[8 * cc + 0] = t0.x; v[8 * cc + 1] = t0.y;
-                                v[8 * cc + 2] = t1.x; v[8 * cc + 3] = t1.y;
-                                v[8 * cc + 4] = t2.x; v[8 * cc + 5] = t2.y;
-                                v[8 * cc + 6] = t3.x; v[8 * cc + 7] = t3.y;
-                            }
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                a00 = fma(v[2 * j], wv[j].x, a00);
-                                a01 = fma(v[2 * j + 1], wv[j].y, a01);
-                                a10 = fma(v[8 + 2 * j], wv[j].x, a10);
-                                a11 = fma(v[8 + 2 * j + 1], wv[j].y, a11);
-                            }
                             int ps = pslot + i;
                             if (ps >= np) ps -= np;
-                            if (ps < SQ) {
-                                const uint32_t t = tq + (uint32_t)(ps * 2 * CS + 2 * 16 * cb);
-                                tmem_st8(t, v);
-                                tmem_st8(t + 16, v + 8);
-                            } else {
-                                double* hp = myhold + (size_t)(ps - SQ) * HSLOT + cb * 16 * 32 + lane;
 #pragma unroll
-                                for (int c = 0; c < 16; ++c) hp[c * 32] = v[c];
+                            for (int hf = 0; hf < NH; ++hf) {
+                                if (hf > 0 && UC * cb + 16 * hf >= bhh) break;  // (no block columns in this half)
+                                const double* a = mystage + (size_t)st * UNIT + hf * 16 * 32 + lbase;
+                                double v[16];  // v[8 cc + 2 j + t] = A[row 2 (rq + 4 (j ^ par)) + t][column 2 co + cc]
+#pragma unroll
+                                for (int cc = 0; cc < 2; ++cc) {
+                                    const double2 t0 = *reinterpret_cast<const double2*>(a + 32 * cc + o0);
+                                    const double2 t1 = *reinterpret_cast<const double2*>(a + 32 * cc + o1);
+                                    const double2 t2 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o0);
+                                    const double2 t3 = *reinterpret_cast<const double2*>(a + 32 * cc + 16 + o1);
+                                    v[8 * cc + 0] = t0.x; v[8 * cc + 1] = t0.y;
+                                    v[8 * cc + 2] = t1.x; v[8 * cc + 3] = t1.y;
+                                    v[8 * cc + 4] = t2.x; v[8 * cc + 5] = t2.y;
+                                    v[8 * cc + 6] = t3.x; v[8 * cc + 7] = t3.y;
+                                }
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    acc[hf][0] = fma(v[2 * j], wv[j].x, acc[hf][0]);
+                                    acc[hf][1] = fma(v[2 * j + 1], wv[j].y, acc[hf][1]);
+                                    acc[hf][2] = fma(v[8 + 2 * j], wv[j].x, acc[hf][2]);
+                                    acc[hf][3] = fma(v[8 + 2 * j + 1], wv[j].y, acc[hf][3]);
+                                }
+                                const int cb16 = NH * cb + hf;  // 16-column block of the sub-sequence
+                                if (ps < SQ) {
+                                    const uint32_t t = tq + (uint32_t)(ps * 2 * CS + 2 * 16 * cb16);
+                                    tmem_st8(t, v);
+                                    tmem_st8(t + 16, v + 8);
+                                } else {
+                                    double* hp = myhold + (size_t)(ps - SQ) * HSLOT + cb16 * 16 * 32 + lane;
+#pragma unroll
+                                    for (int c = 0; c < 16; ++c) hp[c * 32] = v[c];
+                                }
                             }
                             sp.mark(2);
                             __syncwarp();       // every lane's reads of the stage are done
@@ -414,12 +430,13 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                         sp.mark(3);
                         // columns 2 co, 2 co + 1 summed over the four rq lanes: lanes with rq & 1 == c
                         // end with column 2 co + c
-                        {
-                            const double s0 = a00 + a01, s1 = a10 + a11;
+#pragma unroll
+                        for (int hf = 0; hf < NH; ++hf) {
+                            const double s0 = acc[hf][0] + acc[hf][1], s1 = acc[hf][2] + acc[hf][3];
                             const bool up = (lane & 1) != 0;
                             double cs_ = (up ? s1 : s0) + __shfl_xor_sync(0xffffffffu, up ? s0 : s1, 1);
                             cs_ += __shfl_xor_sync(0xffffffffu, cs_, 2);
-                            if (rq < 2) pdst[cb * 16 + 2 * co + rq] = cs_;
+                            if (rq < 2 && (NH * cb + hf) * 16 < CS) pdst[(NH * cb + hf) * 16 + 2 * co + rq] = cs_;
                         }
                         sp.mark(7);
                     }
