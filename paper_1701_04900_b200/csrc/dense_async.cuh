@@ -444,10 +444,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 const long long nr = (P.m - r0) < R ? (P.m - r0) : R;
                 const uint32_t rbytes = (uint32_t)(((nr + 1) & ~1ll) * 8);
                 double* dst = stages + st * STAGE;
+#ifdef ASY_DIAG_NO_RB
+                // (measurement only: no residual / b rows -- the results are meaningless)
+                mbar_arrive_expect_tx(&full[st], box_bytes);
+                tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
+#else
                 mbar_arrive_expect_tx(&full[st], box_bytes + 2 * rbytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
                 bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
                 bulk_g2s_nohint(dst + PANEL + R, P.aux + r0, rbytes, &full[st]);
+#endif
             }
         }
         __syncwarp();
