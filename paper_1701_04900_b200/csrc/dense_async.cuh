@@ -449,10 +449,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
                 mbar_arrive_expect_tx(&full[st], box_bytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
 #else
-                mbar_arrive_expect_tx(&full[st], box_bytes + 2 * rbytes);
+                // (least squares: phi'(r) = 2 s r needs no b rows -- r = Ax - b already holds them --
+                // so the panel costs two bulk copies instead of three)
+                constexpr uint32_t ncopy = LOSS == LOSS_LS ? 1u : 2u;
+                mbar_arrive_expect_tx(&full[st], box_bytes + ncopy * rbytes);
                 tma_load_2d(dst, &tmap, (int)r0, (int)(e.b * P.B), &full[st], pol);
                 bulk_g2s_nohint(dst + PANEL, P.r + r0, rbytes, &full[st]);
-                bulk_g2s_nohint(dst + PANEL + R, P.aux + r0, rbytes, &full[st]);
+                if constexpr (LOSS != LOSS_LS) bulk_g2s_nohint(dst + PANEL + R, P.aux + r0, rbytes, &full[st]);
 #endif
             }
         }
