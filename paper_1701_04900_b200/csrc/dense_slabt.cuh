@@ -511,6 +511,11 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                             for (int e = 0; e < 8; ++e) s8[e] = fma(t[(c32 + 8 + e) * 32], d2.y, s8[e]);
                         }
                     }
+                    // the park slot is free as soon as every lane holds its elements' products (the
+                    // row sums below and the residual update do not read it)
+                    __syncwarp();
+                    ++fin;
+                    if (lane == 0) st_release_cta_u32(&parked_done[a], fin);
                     // sum over the eight co lanes (transposing butterfly): lane bit 2 pairs the two
                     // row-pair orders (my j = 0, 2 are the partner's j = 1, 3), bits 3 and 4 split the
                     // remaining four rows; the lane ends with the total of row
@@ -530,9 +535,6 @@ __global__ void __launch_bounds__(kSlabThreads, 1)
                         else if (h < NSPLIT - 1) delta[srow] += part;
                         else rs[srow] += delta[srow] + part;  // the whole block update at once
                     }
-                    __syncwarp();
-                    ++fin;
-                    if (lane == 0) st_release_cta_u32(&parked_done[a], fin);
                 }
                 pslot += cnt;
                 if (pslot >= np) pslot -= np;
